@@ -1,0 +1,484 @@
+"""CPU oracle for Fate's offloaded-MoE hot path (arXiv 2502.12224).
+
+TEST INFRASTRUCTURE ONLY.  Nothing in ``paper_2502_12224_b200`` imports this
+module; only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may use it, and only as the
+checker or as the timed CPU baseline.
+
+This is a numpy restatement of the reference's arithmetic for the path the
+B200 framework executes.  Each function cites the reference ``moesim`` source
+it follows (paths relative to ``/root/reference/pkg/src/moesim``).  Parity is
+PINNED: ``tests/test_oracle_golden.py`` checks every function here against
+golden vectors produced by running the reference itself
+(``tests/golden/make_golden.py``), including the full per-step decode and
+prefill schedules of ``pipeline.simulate_decoding`` / ``simulate_prefill``.
+
+The reference has no expert FFN (it is a time constant, pipeline.py:477-479);
+``ffn_swiglu`` is the repo's own fp64 definition of the expert compute the GPU
+path executes and is pinned only by construction.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# ---------------------------------------------------------------------------
+# Gate, top-k, cross-layer prediction
+
+
+def softmax64(z: np.ndarray) -> np.ndarray:
+    """Max-subtracted fp64 softmax (gatesim.py:106-110)."""
+    z = np.asarray(z, dtype=np.float64)
+    ez = np.exp(z - z.max())
+    return ez / ez.sum()
+
+
+def gate_routing(mat: np.ndarray, tau: float, h: np.ndarray) -> np.ndarray:
+    """softmax(W_l h / tau_l) in fp64 (gatesim.py:113-123)."""
+    return softmax64((np.asarray(mat, np.float64) @ np.asarray(h, np.float64)) / tau)
+
+
+def rank_order(w: np.ndarray) -> list[int]:
+    """Experts sorted by (-w, id): the tie rule of core.py:159-163 and predict.py:80."""
+    w = np.asarray(w)
+    return [int(i) for i in np.lexsort((np.arange(w.shape[0]), -w))]
+
+
+def top_k(w: np.ndarray, k: int) -> list[int]:
+    """Top-k ids in rank order (core.py:159-163 returns the same set)."""
+    return rank_order(w)[:k]
+
+
+def nearest_rank_threshold(w: np.ndarray, q: float) -> float:
+    """Value at rank ceil(q*n) of the ascending sample (predict.py:84-89)."""
+    s = np.sort(np.asarray(w))
+    r = min(max(int(math.ceil(q * s.shape[0])), 1), s.shape[0])
+    return float(s[r - 1])
+
+
+def predicted_list(w: np.ndarray, kind: str, q: float, k: int) -> list[int]:
+    """Ordered prediction list of cross_layer_predict (predict.py:92-107).
+
+    topk: the k best.  percentile: {w > thr} | top-k, sorted by (-w, id).
+    """
+    order = rank_order(w)
+    if kind == "topk":
+        return order[:k]
+    thr = nearest_rank_threshold(w, q)
+    keep = set(order[:k]) | {int(e) for e in np.nonzero(np.asarray(w) > thr)[0]}
+    return [e for e in order if e in keep]
+
+
+def transfer_budget(t_moe: float, t_attn: float, t_gate: float, t_io: float) -> int:
+    """n = floor((t_moe + t_attn + t_gate) / t_io) (pipeline.py:151-156)."""
+    return math.floor((t_moe + t_attn + t_gate) / t_io)
+
+
+# ---------------------------------------------------------------------------
+# Capacity plan and ARC
+
+
+def plan_capacities(num_layers: int, num_experts: int, boundary: int, cache_total: int) -> list[int]:
+    """Shallow-favoring split of ``cache_total`` slots (cache.py:42-74)."""
+    cap = [0] * num_layers
+    left = cache_total
+    for layer in range(min(boundary, num_layers)):
+        if left == 0:
+            break
+        cap[layer] = min(num_experts, left)
+        left -= cap[layer]
+    n_deep = num_layers - boundary
+    if left > 0 and n_deep > 0:
+        per = min(num_experts, left // n_deep)
+        spare = left - per * n_deep if per < num_experts else 0
+        for layer in range(boundary, num_layers):
+            cap[layer] = per + (1 if layer - boundary < spare else 0)
+    return cap
+
+
+def slots_for_budget(budget: int, dense_bytes: int, slot_bytes: int) -> int:
+    """(budget - dense) // expert_bytes[cached_bits] (cache.py:32-39)."""
+    if budget < dense_bytes:
+        raise ValueError("budget below dense footprint")
+    return (budget - dense_bytes) // slot_bytes
+
+
+@dataclass
+class Arc:
+    """One layer's ARC lists, LRU first (cache.py:104-179).
+
+    Restated from Megiddo & Modha's ARC as the reference realises it: the
+    replace() rule of cache.py:128-135 and the four access cases of
+    cache.py:137-179 (T hit, B1 ghost, B2 ghost, full miss IV-A / IV-B).
+    """
+
+    c: int
+    t1: list = field(default_factory=list)
+    t2: list = field(default_factory=list)
+    b1: list = field(default_factory=list)
+    b2: list = field(default_factory=list)
+    p: float = 0.0
+
+    def resident(self) -> set:
+        return set(self.t1) | set(self.t2)
+
+    def _evict_one(self, x: int) -> int | None:
+        """REPLACE: demote the LRU of T1 or T2 to its ghost list; returns the victim."""
+        n1 = len(self.t1)
+        if n1 and (n1 > self.p or (x in self.b2 and n1 == self.p)):
+            v = self.t1.pop(0)
+            self.b1.append(v)
+            return v
+        if self.t2:
+            v = self.t2.pop(0)
+            self.b2.append(v)
+            return v
+        if self.t1:
+            v = self.t1.pop(0)
+            self.b1.append(v)
+            return v
+        return None
+
+    def access(self, x: int) -> tuple[bool, int | None]:
+        """Returns (hit, victim removed from residency or None)."""
+        c = self.c
+        if c < 1:
+            return False, None
+        if x in self.t1 or x in self.t2:
+            (self.t1 if x in self.t1 else self.t2).remove(x)
+            self.t2.append(x)
+            return True, None
+        if x in self.b1:
+            self.p = min(float(c), self.p + max(1.0, len(self.b2) / len(self.b1)))
+            v = self._evict_one(x)
+            self.b1.remove(x)
+            self.t2.append(x)
+            return False, v
+        if x in self.b2:
+            self.p = max(0.0, self.p - max(1.0, len(self.b1) / len(self.b2)))
+            v = self._evict_one(x)
+            self.b2.remove(x)
+            self.t2.append(x)
+            return False, v
+        v = None
+        if len(self.t1) + len(self.b1) == c:
+            if len(self.t1) < c:
+                self.b1.pop(0)
+                v = self._evict_one(x)
+            else:
+                v = self.t1.pop(0)
+        else:
+            tot = len(self.t1) + len(self.b1) + len(self.t2) + len(self.b2)
+            if tot >= c:
+                if tot == 2 * c:
+                    self.b2.pop(0)
+                v = self._evict_one(x)
+        self.t1.append(x)
+        return False, v
+
+    def state(self) -> dict:
+        return {"t1": list(self.t1), "t2": list(self.t2), "b1": list(self.b1),
+                "b2": list(self.b2), "p": float(self.p)}
+
+
+def seed_arc(arc: Arc, experts) -> None:
+    """LayeredExpertCache.seed_resident (cache.py:197-204)."""
+    for e in experts:
+        if len(arc.t1) + len(arc.t2) >= arc.c:
+            break
+        if int(e) not in arc.resident():
+            arc.t1.append(int(e))
+
+
+# ---------------------------------------------------------------------------
+# Group-wise affine quantization (quant.py:30-120), vectorised
+
+
+def pack_codes(codes: np.ndarray, bits: int) -> np.ndarray:
+    """Little-endian-in-byte packing: element i of a byte at bit i*bits (quant.py:30-39)."""
+    per = 8 // bits
+    c = np.asarray(codes, dtype=np.uint8).reshape(-1)
+    pad = (-c.shape[0]) % per
+    if pad:
+        c = np.concatenate([c, np.zeros(pad, np.uint8)])
+    c = c.reshape(-1, per).astype(np.uint16)
+    shifts = (np.arange(per, dtype=np.uint16) * bits)
+    return (c << shifts).sum(axis=1).astype(np.uint8)
+
+
+def unpack_codes(packed: np.ndarray, bits: int, n: int) -> np.ndarray:
+    """Inverse of pack_codes (quant.py:42-48)."""
+    per = 8 // bits
+    p = np.asarray(packed, dtype=np.uint8).reshape(-1, 1)
+    shifts = (np.arange(per, dtype=np.uint8) * bits).reshape(1, -1)
+    return ((p >> shifts) & ((1 << bits) - 1)).reshape(-1)[:n].astype(np.uint8)
+
+
+def quantize(w: np.ndarray, bits: int, group: int = 64):
+    """Min/max affine group quantization, round-half-even (quant.py:67-107).
+
+    Returns (packed codes uint8, scales f64, zeros f64).  Vectorised over
+    groups; a short tail group is handled separately so the arithmetic per
+    element is exactly the reference's fp64 sequence.
+    """
+    flat = np.asarray(w, dtype=np.float64).reshape(-1)
+    n = flat.shape[0]
+    levels = (1 << bits) - 1
+    n_groups = max(1, math.ceil(n / group))
+    scales = np.zeros(n_groups)
+    zeros = np.zeros(n_groups)
+    codes = np.zeros(n, dtype=np.uint8)
+    full = n // group
+
+    def _do(x: np.ndarray):
+        mn = x.min(axis=1)
+        mx = x.max(axis=1)
+        rng = mx - mn
+        sc = np.where(rng == 0.0, 0.0, rng / levels)
+        safe = np.where(sc == 0.0, 1.0, sc)
+        q = np.rint((x - mn[:, None]) / safe[:, None])
+        q = np.where((sc == 0.0)[:, None], 0.0, np.clip(q, 0, levels))
+        return mn, sc, q.astype(np.uint8)
+
+    if full:
+        mn, sc, q = _do(flat[: full * group].reshape(full, group))
+        zeros[:full], scales[:full] = mn, sc
+        codes[: full * group] = q.reshape(-1)
+    if n > full * group:
+        mn, sc, q = _do(flat[full * group:].reshape(1, -1))
+        zeros[full], scales[full] = mn[0], sc[0]
+        codes[full * group:] = q.reshape(-1)
+    return pack_codes(codes, bits), scales, zeros
+
+
+def dequantize(packed, scales, zeros, bits: int, shape, group: int = 64) -> np.ndarray:
+    """zero + code*scale in fp64 (quant.py:110-120)."""
+    n = int(np.prod(shape))
+    c = unpack_codes(packed, bits, n).astype(np.float64)
+    gi = np.arange(n) // group
+    return (np.asarray(zeros, np.float64)[gi] + c * np.asarray(scales, np.float64)[gi]).reshape(shape)
+
+
+def expert_bytes(n_params: int, bits: int, group: int = 64) -> int:
+    """Packed size ceil(n*b/8) + 8*ceil(n/group) (quant.py:239-246); bf16 = 2n."""
+    if bits == 16:
+        return 2 * n_params
+    return math.ceil(n_params * bits / 8) + 8 * math.ceil(n_params / group)
+
+
+# ---------------------------------------------------------------------------
+# Popularity and bit assignment (quant.py:123-185, predict.py:179-195)
+
+
+def popularity(lists) -> tuple[dict, list]:
+    """counts[e] = #lists containing e; ordering by (-count, id)."""
+    counts: dict[int, int] = {}
+    for lst in lists:
+        for e in set(int(x) for x in lst):
+            counts[e] = counts.get(e, 0) + 1
+    order = sorted(counts, key=lambda e: (-counts[e], e))
+    return counts, order
+
+
+def assign_bits_prefill(order: list, p_int2: float) -> dict:
+    """floor(p*|active|) least popular -> 2 bits, rest 4 (quant.py:168-185)."""
+    m = math.floor(p_int2 * len(order))
+    low = set(order[len(order) - m:]) if m > 0 else set()
+    return {e: (2 if e in low else 4) for e in order}
+
+
+# ---------------------------------------------------------------------------
+# Expert FFN (repo-defined; the reference has none)
+
+
+def silu(x):
+    return x / (1.0 + np.exp(-x))
+
+
+def ffn_swiglu(x: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> np.ndarray:
+    """W2 (silu(W1 x) * (W3 x)) in fp64.  x [..., H]; w1,w3 [I, H]; w2 [H, I]."""
+    x = np.asarray(x, np.float64)
+    a = silu(x @ np.asarray(w1, np.float64).T) * (x @ np.asarray(w3, np.float64).T)
+    return a @ np.asarray(w2, np.float64).T
+
+
+# ---------------------------------------------------------------------------
+# Timing-independent decode / prefill schedules
+
+
+@dataclass
+class StrategyKnobs:
+    """The Strategy fields the schedule reads (pipeline.py:44-104)."""
+
+    kind: str = "fate"            # fate | eap | lod
+    policy_kind: str = "percentile"
+    q: float = 0.75
+    quant: bool = True            # quant_policy is not None
+    p_int2: float = 0.25
+    decode_bits: int = 4
+    cache_bits: int = 4
+    reorder_prefill: bool = True
+
+    @property
+    def prefetch_bits(self) -> int:
+        return self.decode_bits if self.quant else 16
+
+    @property
+    def ondemand_bits(self) -> int:
+        return 2 if self.quant else 16
+
+
+def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
+                    knobs: StrategyKnobs, cached_bits: int, arcs: list | None = None) -> dict:
+    """Timing-independent fields of simulate_decoding (pipeline.py:343-517).
+
+    gate_in [T, L, H] fp64, chosen [T][L] ids.  Per (token, layer) step:
+    predicted list for layer+1 truncated to n (pipeline.py:390-393), the
+    prefetch-issued set (skip resident, :397), cache-hit flags (:442),
+    on-demand set (:450-459), source bits (:444, :453, :459), the ARC victims
+    of update_after_layer (:483) and the recall contribution (:433-436).
+    """
+    T, L = len(chosen), len(chosen[0])
+    arcs = arcs if arcs is not None else [Arc(c) for c in caps]
+    issued: dict = {}
+    pred_sets: dict = {}
+    steps = []
+    recall_sum, recall_n, dequant = 0.0, 0, 0
+    cache_hits = 0
+    use_pred = knobs.kind == "fate"
+    for t in range(T):
+        for l in range(L):
+            rec = {"token": t, "layer": l}
+            if use_pred and l + 1 < L:
+                w = gate_routing(mats[l + 1], taus[l + 1], gate_in[t][l])
+                lst = predicted_list(w, knobs.policy_kind, knobs.q, k)[:budget_n]
+                pred_sets[(t, l + 1)] = set(lst)
+                iss = [e for e in lst if e not in arcs[l + 1].resident()]
+                issued[(t, l + 1)] = iss
+                rec["pred"] = lst
+                rec["prefetch"] = iss
+            ch = sorted(int(e) for e in chosen[t][l])
+            rec["chosen"] = ch
+            if (t, l) in pred_sets:
+                recall_sum += len(pred_sets.pop((t, l)) & set(ch)) / len(ch)
+                recall_n += 1
+            res = arcs[l].resident()
+            iss_here = set(issued.pop((t, l), []))
+            hits, od, src = [], [], []
+            for e in ch:
+                if e in res:
+                    hits.append(e)
+                    src.append(cached_bits if cached_bits < 16 else 16)
+                elif e in iss_here:
+                    src.append(knobs.prefetch_bits)
+                else:
+                    od.append(e)
+                    src.append(knobs.ondemand_bits)
+            cache_hits += len(hits)
+            dequant += sum(1 for b in src if b < 16)
+            victims = []
+            for e in ch:
+                _, v = arcs[l].access(e)
+                if v is not None:
+                    victims.append(v)
+            rec.update({"hits": hits, "ondemand": od, "src_bits": src, "victims": victims})
+            steps.append(rec)
+    return {"steps": steps, "recall": (recall_sum / recall_n) if recall_n else 0.0,
+            "dequant_count": dequant, "cache_hits": cache_hits,
+            "accesses": T * L * k, "arcs": [a.state() for a in arcs]}
+
+
+def prefill_schedule(gate_in, chosen, mats, taus, caps, k: int, knobs: StrategyKnobs,
+                     cached_bits: int, started: dict | None = None, arcs: list | None = None) -> dict:
+    """Timing-independent fields of simulate_prefill (pipeline.py:536-778).
+
+    ``started[layer]`` is the set of that layer's prefetches that had begun
+    by the layer's block end (timing-dependent: pipeline.py:682 drops the
+    rest, which are then fetched on demand at ondemand_bits, :701-719).  When
+    ``None`` every issued prefetch counts as started.
+    """
+    T, L = len(chosen), len(chosen[0])
+    arcs = arcs if arcs is not None else [Arc(c) for c in caps]
+    issued: dict = {}
+    profiles: dict = {}
+    layers = []
+    recall_sum, recall_n, dequant = 0.0, 0, 0
+    for l in range(L):
+        rec = {"layer": l}
+        if knobs.kind == "fate" and l + 1 < L:
+            lists = []
+            for t in range(T):
+                w = gate_routing(mats[l + 1], taus[l + 1], gate_in[t][l])
+                lists.append(top_k(w, k))
+            counts, order = popularity(lists)
+            bits = assign_bits_prefill(order, knobs.p_int2) if knobs.quant else {e: 16 for e in order}
+            if not knobs.reorder_prefill:
+                seen, order_iss = set(), []
+                for lst in lists:
+                    for e in sorted(lst):
+                        if e not in seen:
+                            seen.add(e)
+                            order_iss.append(e)
+            else:
+                order_iss = order
+            res_next = arcs[l + 1].resident()
+            iss = [(e, bits[e]) for e in order_iss if e not in res_next]
+            issued[l + 1] = iss
+            profiles[l + 1] = (counts, order)
+            rec.update({"pred_order": order, "pred_counts": [counts[e] for e in order],
+                        "prefetch": iss})
+        counts = {}
+        for t in range(T):
+            for e in chosen[t][l]:
+                counts[int(e)] = counts.get(int(e), 0) + 1
+        actives = sorted(counts)
+        rec["actives"] = actives
+        rec["counts"] = [counts[e] for e in actives]
+        if l in profiles:
+            pc, po = profiles.pop(l)
+            recall_sum += len(set(po) & set(actives)) / len(actives)
+            recall_n += 1
+        res = arcs[l].resident()
+        iss_here = dict(issued.pop(l, []))
+        st = iss_here.keys() if started is None else set(started.get(l, ()))
+        resident, planned, unplanned = [], [], []
+        src = {}
+        for e in actives:
+            if e in res:
+                resident.append(e)
+                src[e] = cached_bits if cached_bits < 16 else 16
+            elif e in iss_here and e in st:
+                planned.append(e)
+                src[e] = iss_here[e]
+            else:
+                unplanned.append(e)
+        od_bits = knobs.ondemand_bits if knobs.kind == "fate" else 16
+        by_pop = lambda e: (-counts[e], e)
+        first_seen, seen = [], set()
+        for t in range(T):
+            for e in sorted(int(x) for x in chosen[t][l]):
+                if e not in seen:
+                    seen.add(e)
+                    first_seen.append(e)
+        unp = set(unplanned)
+        od_order = (sorted(unplanned, key=by_pop) if knobs.reorder_prefill
+                    else [e for e in first_seen if e in unp])
+        for e in od_order:
+            src[e] = od_bits
+        dequant += sum(1 for e in actives if src[e] < 16)
+        rec.update({"resident": resident, "planned": planned, "ondemand": od_order,
+                    "src_bits": [src[e] for e in actives],
+                    "compute_order": (sorted(resident, key=by_pop) + sorted(planned, key=by_pop) + od_order)
+                    if knobs.reorder_prefill else first_seen})
+        victims = []
+        for e in actives:
+            _, v = arcs[l].access(e)
+            if v is not None:
+                victims.append(v)
+        rec["victims"] = victims
+        layers.append(rec)
+    return {"layers": layers, "recall": (recall_sum / recall_n) if recall_n else 0.0,
+            "dequant_count": dequant, "arcs": [a.state() for a in arcs]}
