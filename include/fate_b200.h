@@ -1,0 +1,232 @@
+/*
+ * fate_b200.h — C ABI of the B200-native Fate offloaded-MoE hot path.
+ *
+ * The reference (moesim, /root/reference/pkg/src/moesim) is a pure-Python
+ * package with no FFI; its "plugin boundary" is the Python API plus the two
+ * injection seams of the engine entry points (pipeline.py:343-353 and
+ * pipeline.py:536-545).  Every entry point below replaces one reference
+ * function (cited per declaration); the Python package
+ * paper_2502_12224_b200 binds them with ctypes.
+ *
+ * Conventions
+ *   - every function returns an int status: FATE_OK or one of FATE_E*; the
+ *     Python wrapper maps these onto the reference's SimError classes;
+ *   - buffers are caller-owned; "_dev" pointers are CUDA device pointers,
+ *     "_host" pointers are host memory (pinned where stated);
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *   - no C++ exception crosses this boundary; no allocation in hot calls
+ *     except inside fate_engine_create.
+ */
+#ifndef FATE_B200_H
+#define FATE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FATE_OK 0
+#define FATE_EINVAL 1     /* InvalidConfig            (errors.py:21)  */
+#define FATE_EMISMATCH 2  /* TraceMismatch            (errors.py:39)  */
+#define FATE_EBUDGET 3    /* BudgetTooSmall           (errors.py:63)  */
+#define FATE_ECODES 4     /* CorruptCodes             (errors.py:75)  */
+#define FATE_ECUDA 5      /* CUDA runtime/driver failure               */
+#define FATE_ENOMEM 6     /* device or pinned allocation failed        */
+#define FATE_ETIMEOUT 7   /* engine watchdog fired (copy never landed) */
+
+#define FATE_MAX_EXPERTS 256
+#define FATE_MAX_TOPK 16
+#define FATE_HEADER_BYTES 256
+
+/* ---- library ------------------------------------------------------------ */
+int fate_version(void);
+/* Last error message of the calling thread (never NULL). */
+const char *fate_last_error(void);
+/* Number of visible CUDA devices, 0 if none; nonzero status if the driver is unusable. */
+int fate_device_count(int *count);
+
+/* ---- K5 quantization: quant.py:67-107 (quantize) and :30-39 (_pack) ------
+ * Group-wise min/max affine quantization of w[n] (fp32 on device) with
+ * fp64 arithmetic and round-half-even, groups of `group` consecutive
+ * elements, packed little-endian within each byte.  Writes
+ *   codes_dev   : ceil(n*bits/8) bytes,
+ *   sz_dev      : optional fp32 (scale, zero) pairs per group (device format),
+ *   scale64_dev / zero64_dev : optional fp64 per-group values (reference format).
+ * bits in {8,4,2}.  bits == 16 converts to bf16 into codes_dev (2n bytes). */
+int fate_quant_pack(const float *w_dev, int64_t n, int bits, int group, uint8_t *codes_dev,
+                    float *sz_dev, double *scale64_dev, double *zero64_dev, void *stream);
+
+/* Same as fate_quant_pack for fp64 input (the reference quantizes fp64 arrays). */
+int fate_quant_pack64(const double *w_dev, int64_t n, int bits, int group, uint8_t *codes_dev, float *sz_dev,
+                      double *scale64_dev, double *zero64_dev, void *stream);
+
+/* dequantize (quant.py:110-120): out[n] fp32 = zero + code*scale from the
+ * device format (fp32 scale/zero); bits 16 reads bf16. */
+int fate_dequant(const uint8_t *codes_dev, const float *sz_dev, int64_t n, int bits, int group,
+                 float *out_dev, void *stream);
+
+/* Pack one expert (w1 [I,H], w3 [I,H], w2 [H,I], fp32 on device) into the
+ * engine's self-describing buffer layout: 256-byte header + payload of
+ * exactly expert_bytes[bits] bytes (quant.py:239-246 formula).  Returns
+ * the payload layout via fate_expert_layout. */
+int fate_pack_expert(const float *w1_dev, const float *w3_dev, const float *w2_dev, int H, int I, int bits,
+                     int layer, int expert, uint8_t *dst_dev, void *stream);
+/* Byte size of one packed expert buffer (header + payload) for (H, I, bits). */
+int64_t fate_expert_buffer_bytes(int H, int I, int bits);
+
+/* ---- K1 gate + cross-layer predictor --------------------------------------
+ * gatesim.py:113-123 (gate_forward), core.py:159-163 (top_k_set),
+ * predict.py:84-107 (nearest_rank_percentile, cross_layer_predict).
+ * For T hidden vectors h[T,H] (fp64): routing[T,E] = softmax(W h / tau) in
+ * fp64; order[T,E] = experts sorted by (-routing, id); list_len[T] = length
+ * of the policy's prediction prefix of `order` (policy 0 = top-k: k;
+ * policy 1 = percentile q: max(k, #{w > nearest-rank(q)})). */
+int fate_gate_forward(const double *W_dev, double tau, const double *h_dev, int T, int E, int H,
+                      double *routing_dev, int32_t *order_dev, int32_t *list_len_dev, int top_k,
+                      int policy, double q, void *stream);
+
+/* ---- K3 decode expert FFN (replaces the t_moe charge, pipeline.py:477-479)
+ * y[H] = sum_j weight[j] * W2_j (silu(W1_j x) * (W3_j x)) over n experts
+ * whose packed buffers (fate_pack_expert layout) are at bufs[j] (device
+ * pointers, host array).  fp32 accumulation.  scratch_dev >= sum_j I_j floats. */
+int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *const *bufs, const float *weights,
+                    float *scratch_dev, float *y_dev, void *stream);
+
+/* ---- K4 prefill grouped expert FFN (replaces pipeline.py:733-750) ----------
+ * For T tokens X[T,H] (fp32 on device), n experts: token lists tok_idx
+ * (concatenated, device int32) with per-expert offsets off[n+1] (host) and
+ * routing weights tok_w (device fp32, aligned with tok_idx):
+ *   Y[t] += tok_w * W2_e(silu(W1_e x_t) * W3_e x_t)  (Y zeroed by the caller).
+ * bf16 operands (dequantized in shared memory), fp32 accumulation. */
+int fate_ffn_prefill(const float *X_dev, int T, int H, int n, const uint8_t *const *bufs,
+                     const int32_t *tok_idx_dev, const float *tok_w_dev, const int32_t *off_host,
+                     float *Y_dev, void *stream);
+
+/* ---- Engine: device-resident expert cache + prefetch + compute ------------
+ * The engine owns: the fp64 router weights, a pool of expert buffers on the
+ * GPU (plan slots + staging), the per-layer ARC tables and expert->buffer
+ * maps (cache.py:104-215), pinned host pools (INT2/INT4/INT8/bf16 copies of
+ * every expert), a copy stream and a host copy manager thread
+ * (the transfer channel, pipeline.py:163-264). */
+typedef struct fate_engine fate_engine;
+
+typedef struct fate_engine_config {
+  int num_layers, num_experts, top_k, hidden_dim, intermediate_dim;
+  int shared_intermediate;       /* 0 = no shared expert                    */
+  int shared_bits;               /* 16, 8, 4 or 2                           */
+  const int32_t *capacity;       /* [num_layers] CachePlan.per_layer_capacity */
+  int cached_bits;               /* CachePlan.cached_bits (reported src bits) */
+  int prefetch_bits;             /* Strategy.prefetch_bits()   (pipeline.py:96-97)  */
+  int ondemand_bits;             /* Strategy.ondemand_bits()   (pipeline.py:99-101) */
+  int use_predictor;             /* fate: 1, lod: 0                         */
+  int policy;                    /* 0 topk, 1 percentile (predict.py:21-47) */
+  double percentile_q;
+  int budget_n;                  /* transfer_budget (pipeline.py:151-156)   */
+  int prefill_use_predictor;     /* fate prefill prediction (pipeline.py:568) */
+  int reorder_prefill;           /* Strategy.reorder_prefill                */
+  double p_int2;                 /* QuantPolicy.p_int2 (prefill INT2 share) */
+  int prefill_ondemand_bits;     /* 2 for fate (pipeline.py:701), 16 otherwise */
+  int max_tokens;                /* decode/prefill capacity for scratch     */
+  int max_inflight;              /* copy-engine issue depth (preemption granularity) */
+  int device;
+} fate_engine_config;
+
+int fate_engine_create(const fate_engine_config *cfg, fate_engine **out);
+int fate_engine_destroy(fate_engine *eng);
+/* Change the Strategy knobs (pipeline.py:44-104) of an existing engine,
+ * keeping its cache state (compare_strategies chaining, pipeline.py:835-850). */
+int fate_engine_set_strategy(fate_engine *eng, const fate_engine_config *cfg);
+/* Timeline of the last timed run (pipeline.py:107-132): step_ms[4*s..] =
+ * gate start, gate end, moe start, moe end (ms from the run start);
+ * copy_ms[2*c..] = start, end; copy_meta[5*c..] = kind (0 prefetch,
+ * 1 on-demand), step, layer, expert, bits.  counts = {steps, copies}. */
+int fate_engine_timeline(fate_engine *eng, double *step_ms, int max_steps, double *copy_ms, int32_t *copy_meta,
+                         int max_copies, int32_t *counts);
+
+/* Router weights W[L,E,H] fp64 and temperatures tau[L] (host arrays; copied). */
+int fate_engine_set_gate(fate_engine *eng, const double *W_host, const double *tau_host);
+/* Register the pinned host pool for one bit width: experts (l,e) at
+ * base + (l*E + e) * stride, each a packed buffer (header + payload). */
+int fate_engine_set_host_pool(fate_engine *eng, int bits, const uint8_t *base_host, int64_t stride);
+/* Shared expert for layer l: a packed device buffer (resident, dense bytes). */
+int fate_engine_set_shared(fate_engine *eng, int layer, const uint8_t *buf_dev);
+
+/* Cache control: LayeredExpertCache(plan) fresh state (cache.py:185-187),
+ * seed_resident (cache.py:197-204; loads the experts' cached_bits copies). */
+int fate_engine_reset_cache(fate_engine *eng);
+int fate_engine_seed_resident(fate_engine *eng, int layer, const int32_t *experts, int n);
+/* contains() (cache.py:192-195) for every expert of a layer: out[E] in {0,1}. */
+int fate_engine_resident(fate_engine *eng, int layer, int32_t *out_host);
+/* Standalone ARC accesses in order (update_after_layer, cache.py:212-215):
+ * hits_host[n] receives 1 on a resident hit.  Buffers of newly inserted
+ * experts are loaded from the cached_bits host pool synchronously. */
+int fate_engine_access(fate_engine *eng, int layer, const int32_t *experts, int n, int32_t *hits_host);
+/* ARC state export: lists LRU-first; lens[4] = |T1|,|T2|,|B1|,|B2|; each list
+ * array must hold num_experts entries. */
+int fate_engine_arc_state(fate_engine *eng, int layer, int32_t *t1, int32_t *t2, int32_t *b1,
+                          int32_t *b2, int32_t *lens, double *p);
+
+/* Per-step parity log (timing-independent fields of pipeline.py:406-490). */
+typedef struct fate_step_log {
+  int32_t chosen[FATE_MAX_TOPK];           /* ascending                          */
+  int32_t src_bits[FATE_MAX_TOPK];         /* source bits per chosen expert      */
+  int32_t hit[FATE_MAX_TOPK];              /* 1 if cache-resident at gate time   */
+  int32_t ondemand[FATE_MAX_TOPK];
+  int32_t victims[FATE_MAX_TOPK];
+  int32_t n_ondemand, n_victims, n_pred, n_prefetch;
+  int32_t arrived[FATE_MAX_TOPK];          /* prefetched AND landed at gate time (timing-dependent) */
+  int32_t pred[FATE_MAX_EXPERTS];          /* entries[:n] for layer+1, rank order */
+  int32_t prefetch[FATE_MAX_EXPERTS];      /* issued (pred minus resident)        */
+  float routing[FATE_MAX_TOPK];            /* fp32 copy of the chosen weights     */
+  int32_t fmt_bits[FATE_MAX_TOPK];         /* storage width of the buffer computed from */
+  int32_t mismatch;                        /* 1 if device top-k != trace chosen   */
+  int32_t pad;
+} fate_step_log;
+
+typedef struct fate_run_stats {
+  double gpu_ms;              /* CUDA-event time of the whole run          */
+  double ffn_ms;              /* summed K3/K4 kernel time (event pairs)    */
+  double gate_ms;             /* summed K1 time                            */
+  int64_t steps, accesses, cache_hits, arrival_hits, dequant_count;
+  int64_t prefetch_issued, ondemand_issued, transfers_done, transfers_dropped;
+  int64_t h2d_bytes;
+  double copy_busy_ms;        /* copy-stream busy time (event pairs)       */
+  double recall_sum; int64_t recall_n;
+  int64_t trace_mismatches;   /* device top-k differing from trace chosen  */
+  int64_t ffn_bytes;          /* algorithmic bytes of executed experts     */
+  double ffn_flops;           /* prefill: 2*3*H*I*tokens summed            */
+  int64_t near_ties;          /* k-th/(k+1)-th weight gap < 1e-12           */
+  int32_t error; int32_t pad;
+} fate_run_stats;
+
+/* Decode T tokens (simulate_decoding, pipeline.py:343-517).
+ * gate_in_dev [T,L,H] fp64 gate inputs, chosen_dev [T,L,k] (trace ids for the
+ * mismatch check, may be NULL); y_dev [T,L,H] fp32 expert outputs;
+ * log_dev [T*L] fate_step_log or NULL.  Blocks until done. */
+int fate_engine_decode(fate_engine *eng, const double *gate_in_dev, const int32_t *chosen_dev, int T,
+                       float *y_dev, fate_step_log *log_dev, fate_run_stats *stats);
+
+/* Per-layer prefill log (timing-independent fields of pipeline.py:608-753). */
+typedef struct fate_prefill_log {
+  int32_t n_pred, n_prefetch, n_active, n_resident, n_planned, n_ondemand, n_victims, n_started;
+  int32_t pred_order[FATE_MAX_EXPERTS], pred_counts[FATE_MAX_EXPERTS];
+  int32_t prefetch[FATE_MAX_EXPERTS], prefetch_bits[FATE_MAX_EXPERTS];
+  int32_t actives[FATE_MAX_EXPERTS], counts[FATE_MAX_EXPERTS];
+  int32_t resident[FATE_MAX_EXPERTS], planned[FATE_MAX_EXPERTS], ondemand[FATE_MAX_EXPERTS];
+  int32_t src_bits[FATE_MAX_EXPERTS];      /* aligned with actives           */
+  int32_t victims[FATE_MAX_EXPERTS];
+  int32_t started[FATE_MAX_EXPERTS];       /* this layer's prefetches that began before block end */
+  int32_t mismatch;
+  int32_t pad;
+} fate_prefill_log;
+
+/* Prefill T tokens (simulate_prefill, pipeline.py:536-778).  Y_dev [L,T,H] fp32. */
+int fate_engine_prefill(fate_engine *eng, const double *gate_in_dev, const int32_t *chosen_dev, int T,
+                        float *Y_dev, fate_prefill_log *log_host, fate_run_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FATE_B200_H */

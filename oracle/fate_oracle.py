@@ -482,3 +482,42 @@ def prefill_schedule(gate_in, chosen, mats, taus, caps, k: int, knobs: StrategyK
         layers.append(rec)
     return {"layers": layers, "recall": (recall_sum / recall_n) if recall_n else 0.0,
             "dequant_count": dequant, "arcs": [a.state() for a in arcs]}
+
+
+# ---------------------------------------------------------------------------
+# Packed expert buffers (the repo's device layout; see csrc/fate_internal.cuh)
+
+
+def buffer_layout(H: int, I: int, bits: int) -> dict:
+    n = H * I
+    if bits == 16:
+        return {"c1": 0, "c3": 2 * n, "c2": 4 * n, "payload": 6 * n}
+    cb, sb = n * bits // 8, n // 64 * 8
+    return {"c1": 0, "c3": cb, "c2": 2 * cb, "s1": 3 * cb, "s3": 3 * cb + sb, "s2": 3 * cb + 2 * sb,
+            "payload": 3 * cb + 3 * sb}
+
+
+def unpack_buffer(buf: np.ndarray, H: int, I: int, bits: int) -> dict:
+    """Split a packed expert buffer into (codes, fp32 sz) per projection and
+    its fp64 dequantized matrices (zero + code*scale with the stored fp32 scale/zero)."""
+    buf = np.asarray(buf, dtype=np.uint8)
+    hdr = buf[:256].view(np.int32)
+    p = buf[256:]
+    lay = buffer_layout(H, I, bits)
+    n = H * I
+    out = {"header": {"bits": int(hdr[1]), "layer": int(hdr[2]), "expert": int(hdr[3]), "H": int(hdr[4]),
+                      "I": int(hdr[5])}}
+    shapes = {"1": (I, H), "3": (I, H), "2": (H, I)}
+    for j in ("1", "3", "2"):
+        c0 = lay["c" + j]
+        if bits == 16:
+            raw = p[c0:c0 + 2 * n].view(np.uint16).astype(np.uint32) << 16
+            out["w" + j] = raw.view(np.float32).astype(np.float64).reshape(shapes[j])
+            continue
+        codes = p[c0:c0 + n * bits // 8]
+        sz = p[lay["s" + j]:lay["s" + j] + n // 64 * 8].view(np.float32).reshape(-1, 2)
+        out["codes" + j] = codes
+        out["sz" + j] = sz
+        out["w" + j] = dequantize(codes, sz[:, 0].astype(np.float64), sz[:, 1].astype(np.float64), bits,
+                                  shapes[j])
+    return out

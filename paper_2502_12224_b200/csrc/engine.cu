@@ -1,0 +1,1213 @@
+// The offload engine: device-resident expert cache + prefetch + compute for
+// decode (simulate_decoding, pipeline.py:343-517) and prefill
+// (simulate_prefill, pipeline.py:536-778) executed on a B200.
+//
+// Per decode step (token t, layer l) on the compute stream:
+//   K1  decode_gate_kernel   fp64 router rows of W_l and W_{l+1} (one CTA per
+//       row), then the last CTA: deferred ARC update of the previous step
+//       (cache.py:212-215), softmax/top-k of layer l, hit / prefetched /
+//       on-demand split (pipeline.py:441-459), cross-layer prediction for
+//       l+1 truncated to n and filtered by residency (pipeline.py:390-404),
+//       the K3 expert batch, and a step message to the host copy manager.
+//   WAIT cuStreamWaitValue32 on a host-mapped flag: set by K1 itself when
+//       every needed expert is already in HBM, otherwise by the host after
+//       the needed copies landed.
+//   K3  ffn_up / ffn_down    dequant-fused SwiGLU over the routed + shared
+//       experts straight from their HBM buffers.
+// The host thread is the transfer channel (pipeline.py:163-264): a FIFO of
+// pending copies with on-demand promotion and stale-prefetch dropping, at
+// most `max_inflight` copies submitted to the copy stream at a time.
+#include <cuda.h>
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "arc_dev.cuh"
+#include "gate_dev.cuh"
+
+namespace fate {
+
+thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_status(cudaError_t e, const char *what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? FATE_ENOMEM : FATE_ECUDA;
+}
+
+// Driver entry points resolved through the runtime (no link-time libcuda
+// dependency, so the library loads on hosts without a driver).
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_wait32 p_wait32 = nullptr;
+static PFN_write32 p_write32 = nullptr;
+
+static int resolve_driver() {
+  if (p_wait32 && p_write32) return FATE_OK;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void *a = nullptr, *b = nullptr;
+  // request the CUDA 12 (v2) ABI of the stream memory operations explicitly
+  if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &a, 12000, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &b, 12000, cudaEnableDefault, &q2) != cudaSuccess ||
+      !a || !b || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess) {
+    g_err = "cannot resolve cuStreamWaitValue32/cuStreamWriteValue32 from the CUDA driver";
+    return FATE_ECUDA;
+  }
+  p_wait32 = (PFN_wait32)a;
+  p_write32 = (PFN_write32)b;
+  return FATE_OK;
+}
+
+static int cu_status(CUresult r, const char *what) {
+  g_err = std::string(what) + ": CUDA driver error " + std::to_string((int)r);
+  return FATE_ECUDA;
+}
+
+#define FATE_CU(call)                                    \
+  do {                                                   \
+    CUresult _r = (call);                                \
+    if (_r != CUDA_SUCCESS) return cu_status(_r, #call); \
+  } while (0)
+
+namespace {
+
+constexpr int kGateThreads = 256;
+
+__device__ __forceinline__ int pop_free(const EngineDev &d) {
+  Ctrl &C = *d.ctrl;
+  if (C.free_top <= 0) {
+    C.err = 1;
+    return 0;
+  }
+  return d.free_stack[--C.free_top];
+}
+
+__device__ __forceinline__ void push_free(const EngineDev &d, int b) {
+  Ctrl &C = *d.ctrl;
+  if (C.free_top >= d.nbuf) {
+    C.err = 2;
+    return;
+  }
+  d.free_stack[C.free_top++] = b;
+}
+
+// Deferred update_after_layer of the previous step: ARC accesses in ascending
+// id order, with buffer hand-over (inserted experts keep the staging buffer
+// they were computed from; evicted experts' buffers return to the free
+// stack).  Warp 0 only.
+__device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_step_log *log, int32_t *rel) {
+  Ctrl &C = *d.ctrl;
+  const int lane = threadIdx.x & 31;
+  const int pl = C.prev_layer;
+  WarpArc arc;
+  arc.load(&d.arc[pl], arc_sm);
+  int nrel = 0, nvic = 0;
+  for (int i = 0; i < C.prev_k; ++i) {
+    const int e = C.prev_chosen[i];
+    int victim;
+    const int hit = arc.access(e, &victim);
+    if (lane == 0) {
+      if (victim >= 0) {
+        int32_t &slot = d.buf_of[pl * d.E + victim];
+        if (slot >= 0) rel[nrel++] = slot;
+        slot = -1;
+        if (log && nvic < KMAX) log[C.prev_step].victims[nvic] = victim;
+        ++nvic;
+      }
+      if (!hit) {
+        const int b = C.prev_buf[i];
+        if (arc.c >= 1) {
+          d.buf_of[pl * d.E + e] = b;
+          for (int r = 0; r < nrel; ++r)
+            if (rel[r] == b) rel[r] = rel[--nrel], r = nrel;
+        } else {
+          rel[nrel++] = b;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  arc.store(&d.arc[pl]);
+  if (lane == 0) {
+    for (int r = 0; r < nrel; ++r) push_free(d, rel[r]);
+    if (log) log[C.prev_step].n_victims = nvic;
+    C.prev_valid = 0;
+  }
+  __syncwarp();
+}
+
+struct TailSmem {
+  ArcLayer arc;
+  double z[2 * EMAX], w[2 * EMAX];
+  int32_t ord[2 * EMAX];
+  int32_t chosen[KMAX], cbuf[KMAX], csrc[KMAX], chit[KMAX], carr[KMAX];
+  int32_t rel[4 * KMAX + 4];
+  int32_t is_chosen[EMAX];
+};
+
+__global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, const double *__restrict__ gate_in,
+                                                                   const int32_t *__restrict__ trace_chosen,
+                                                                   fate_step_log *__restrict__ log, int layer,
+                                                                   volatile uint32_t *ready_host) {
+  __shared__ double red[kGateThreads / 32];
+  __shared__ int is_last;
+  __shared__ TailSmem S;
+  const int E = d.E, H = d.H, L = d.L;
+  const int token = *(volatile int32_t *)&d.ctrl->next_token;
+  const double *h = gate_in + ((int64_t)token * L + layer) * H;
+  const int row = blockIdx.x;
+  const int lrow = row < E ? layer : layer + 1;
+  const int e_row = row < E ? row : row - E;
+  // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
+  {
+    const double *W = d.W + ((int64_t)lrow * E + e_row) * H;
+    double acc = 0.0;
+    const double2 *W2 = reinterpret_cast<const double2 *>(W);
+    const double2 *h2 = reinterpret_cast<const double2 *>(h);
+    for (int i = threadIdx.x; i < H / 2; i += kGateThreads) {
+      const double2 a = __ldg(W2 + i), b = __ldg(h2 + i);
+      acc = fma(a.x, b.x, acc);
+      acc = fma(a.y, b.y, acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kGateThreads / 32; ++w) s += red[w];
+      d.logits[row] = __ddiv_rn(s, d.tau[lrow]);
+      __threadfence();
+      const uint32_t ticket = atomicAdd(&d.ctrl->arrive, 1u);
+      is_last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+  }
+  if (!is_last) return;
+  __threadfence();
+  Ctrl &C = *d.ctrl;
+  // ---- FFN input x = sqrt(H) * gate_in (fp64 product, fp32 storage)
+  const double sH = sqrt((double)H);
+  for (int i = threadIdx.x; i < H; i += kGateThreads) d.x[i] = (float)(sH * h[i]);
+  for (int i = threadIdx.x; i < gridDim.x; i += kGateThreads) S.z[i] = ((volatile double *)d.logits)[i];
+  for (int i = threadIdx.x; i < E; i += kGateThreads) S.is_chosen[i] = 0;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  if (lane == 0) C.arrive = 0;
+  const int k = d.k;
+  const int step = C.step;
+  fate_step_log *lg = log ? log + step : nullptr;
+  // (1) deferred ARC update of the previous step
+  if (C.prev_valid) apply_prev_update(d, &S.arc, log, S.rel);
+  // (2) routing of layer l: softmax + rank (gatesim.py:113-123, core.py:159-163)
+  warp_softmax_rank(S.z, S.w, S.ord, E, k, 0, d.q);
+  if (lane == 0) {
+    for (int i = 0; i < k; ++i) S.chosen[i] = S.ord[i];
+    for (int i = 1; i < k; ++i)  // ascending ids (pipeline.py:441 iterates sorted(chosen))
+      for (int j = i; j > 0 && S.chosen[j - 1] > S.chosen[j]; --j) {
+        const int t = S.chosen[j];
+        S.chosen[j] = S.chosen[j - 1];
+        S.chosen[j - 1] = t;
+      }
+    for (int i = 0; i < k; ++i) S.is_chosen[S.chosen[i]] = 1;
+    int mism = 0;
+    if (trace_chosen) {
+      const int32_t *tc = trace_chosen + ((int64_t)token * L + layer) * k;
+      for (int i = 0; i < k; ++i) mism |= (tc[i] != S.chosen[i]);
+    }
+    if (mism) atomicAdd(&d.stats->mismatches, 1ull);
+    if (k < E && S.w[S.ord[k - 1]] - S.w[S.ord[k]] < 1e-12) atomicAdd(&d.stats->near_ties, 1ull);
+    if (lg) lg->mismatch = mism;
+    // recall of the prediction made one step earlier (pipeline.py:433-436)
+    if (C.pred_valid && C.pred_layer == layer) {
+      int inter = 0;
+      for (int i = 0; i < C.pred_n; ++i) inter += S.is_chosen[C.pred_list[i]];
+      d.stats->recall_sum += (double)inter / (double)k;
+      d.stats->recall_n += 1;
+      C.pred_valid = 0;
+    }
+  }
+  __syncwarp();
+  // (3) hit / prefetched / on-demand split (pipeline.py:441-459)
+  StepMsg *msg = d.ring + (step % kRing);
+  if (lane == 0) {
+    int n_od = 0, n_need = 0, n_hit = 0, n_arr = 0, n_deq = 0;
+    bool all_landed = true;
+    for (int i = 0; i < k; ++i) {
+      const int e = S.chosen[i];
+      int b = d.buf_of[layer * E + e];
+      int src, hit = 0, arr = 0;
+      if (b >= 0) {
+        hit = 1;
+        src = d.cached_bits < 16 ? d.cached_bits : 16;
+      } else if (d.pend_buf[layer * E + e] >= 0) {
+        b = d.pend_buf[layer * E + e];
+        src = d.prefetch_bits;
+        arr = ((volatile uint32_t *)d.buf_done)[b] == d.pend_gen[layer * E + e];
+        all_landed = all_landed && arr;
+        msg->need_e[n_need] = e;
+        msg->need_b[n_need] = b;
+        ++n_need;
+      } else {
+        b = pop_free(d);
+        const uint32_t g = ++d.buf_gen[b];
+        src = d.ondemand_bits;
+        d.buf_bits[b] = d.ondemand_bits;
+        msg->od_e[n_od] = e;
+        msg->od_b[n_od] = b;
+        msg->od_g[n_od] = g;
+        if (lg) lg->ondemand[n_od] = e;
+        ++n_od;
+        all_landed = false;
+      }
+      C.prev_chosen[i] = e;
+      C.prev_buf[i] = b;
+      S.cbuf[i] = b;
+      n_hit += hit;
+      n_arr += arr;
+      n_deq += src < 16;
+      if (lg) {
+        lg->chosen[i] = e;
+        lg->src_bits[i] = src;
+        lg->hit[i] = hit;
+        lg->arrived[i] = arr;
+        lg->routing[i] = (float)S.w[e];
+        lg->fmt_bits[i] = d.buf_bits[b];
+      }
+    }
+    // (4) prefetched-but-not-chosen experts of this layer: release their buffers
+    // and tell the host to drop them if still queued (drop_stale, pipeline.py:438/247-253)
+    int n_drop = 0;
+    for (int e = 0; e < E; ++e) {
+      const int b = d.pend_buf[layer * E + e];
+      if (b < 0) continue;
+      d.pend_buf[layer * E + e] = -1;
+      if (S.is_chosen[e]) continue;
+      msg->drop_e[n_drop] = e;
+      msg->drop_b[n_drop] = b;
+      ++n_drop;
+      push_free(d, b);
+    }
+    msg->n_od = n_od;
+    msg->n_need = n_need;
+    msg->n_drop = n_drop;
+    msg->od_bits = d.ondemand_bits;
+    msg->pf_bits = d.prefetch_bits;
+    if (lg) lg->n_ondemand = n_od;
+    atomicAdd(&d.stats->accesses, (unsigned long long)k);
+    atomicAdd(&d.stats->cache_hits, (unsigned long long)n_hit);
+    atomicAdd(&d.stats->arrival_hits, (unsigned long long)n_arr);
+    atomicAdd(&d.stats->dequant_count, (unsigned long long)n_deq);
+    atomicAdd(&d.stats->ondemand_issued, (unsigned long long)n_od);
+    S.carr[0] = all_landed ? 1 : 0;
+  }
+  __syncwarp();
+  // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
+  int n_pf = 0;
+  if (d.use_predictor && layer + 1 < L) {
+    const int len = warp_softmax_rank(S.z + E, S.w + E, S.ord + E, E, k, d.policy, d.q);
+    if (lane == 0) {
+      const int n = len < d.budget_n ? len : d.budget_n;
+      C.pred_n = n;
+      C.pred_layer = layer + 1;
+      C.pred_valid = 1;
+      for (int i = 0; i < n; ++i) {
+        const int e = S.ord[E + i];
+        C.pred_list[i] = e;
+        if (lg) lg->pred[i] = e;
+        if (d.buf_of[(layer + 1) * E + e] >= 0) continue;  // resident: skip (pipeline.py:397)
+        const int b = pop_free(d);
+        const uint32_t g = ++d.buf_gen[b];
+        d.buf_bits[b] = d.prefetch_bits;
+        d.pend_buf[(layer + 1) * E + e] = b;
+        d.pend_gen[(layer + 1) * E + e] = g;
+        msg->pf_e[n_pf] = e;
+        msg->pf_b[n_pf] = b;
+        msg->pf_g[n_pf] = g;
+        msg->pf_bits_each[n_pf] = d.prefetch_bits;
+        if (lg) lg->prefetch[n_pf] = e;
+        ++n_pf;
+      }
+      if (lg) lg->n_pred = n, lg->n_prefetch = n_pf;
+      atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
+    }
+  } else if (lane == 0 && lg) {
+    lg->n_pred = -1;
+    lg->n_prefetch = 0;
+  }
+  __syncwarp();
+  // (6) the K3 batch: routed experts weighted by their full-softmax routing
+  // weight (not renormalised), plus the shared expert with weight 1.
+  if (lane == 0) {
+    FfnBatch &B = *d.batch;
+    B.H = H;
+    int off = 0, n = 0;
+    for (int i = 0; i < k; ++i) {
+      B.e[n] = FfnExpert{d.pool + (int64_t)S.cbuf[i] * d.buf_stride, (float)S.w[S.chosen[i]], d.I, 0, off};
+      off += d.I;
+      ++n;
+    }
+    if (d.shared && d.shared[layer]) {
+      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, 0, off};
+      off += d.I_shared;
+      ++n;
+    }
+    B.n = n;
+    B.total_I = off;
+    // (7) step message + (8) self-signal when nothing must be waited for
+    msg->n_pf = n_pf;
+    msg->step = step;
+    msg->token = token;
+    msg->layer = layer;
+    const int self = S.carr[0];
+    msg->self_signaled = self;
+    if (self) ready_host[layer] = (uint32_t)token + 1u;
+    __threadfence_system();
+    msg->seq = (uint32_t)step + 1u;
+    __threadfence_system();
+    // (9) control block for the next step
+    C.prev_valid = 1;
+    C.prev_layer = layer;
+    C.prev_k = k;
+    C.prev_step = step;
+    C.cur_token = token;
+    C.cur_layer = layer;
+    C.step = step + 1;
+    if (layer == L - 1) C.next_token = token + 1;
+    __threadfence();
+  }
+}
+
+// Final deferred update (after the last decode step) and standalone access.
+__global__ void arc_flush_kernel(EngineDev d, fate_step_log *log) {
+  __shared__ ArcLayer arc_sm;
+  __shared__ int32_t rel[4 * KMAX + 4];
+  if (d.ctrl->prev_valid) apply_prev_update(d, &arc_sm, log, rel);
+}
+
+// Standalone ARC accesses (update_after_layer / arc_access API).  Newly
+// resident experts get a buffer popped here; their ids + buffers are returned
+// so the host can load the cached_bits copy synchronously.
+__global__ void arc_access_kernel(EngineDev d, int layer, const int32_t *experts, int n, int32_t *hits,
+                                  int32_t *loads /* [2n]: expert, buffer; -1 terminated */) {
+  __shared__ ArcLayer arc_sm;
+  const int lane = threadIdx.x;
+  WarpArc arc;
+  arc.load(&d.arc[layer], &arc_sm);
+  int nl = 0;
+  for (int i = 0; i < n; ++i) {
+    const int e = experts[i];
+    int victim;
+    const int hit = arc.access(e, &victim);
+    if (lane == 0) {
+      hits[i] = hit;
+      if (victim >= 0) {
+        int32_t &slot = d.buf_of[layer * d.E + victim];
+        if (slot >= 0) {
+          push_free(d, slot);
+          for (int j = 0; j < nl; ++j)
+            if (loads[2 * j + 1] == slot) loads[2 * j] = -2;  // loaded then evicted: skip copy
+        }
+        slot = -1;
+      }
+      if (!hit && arc.c >= 1) {
+        const int b = pop_free(d);
+        d.buf_bits[b] = d.cached_bits;
+        d.buf_of[layer * d.E + e] = b;
+        loads[2 * nl] = e;
+        loads[2 * nl + 1] = b;
+        ++nl;
+      }
+    }
+    __syncwarp();
+  }
+  arc.store(&d.arc[layer]);
+  if (lane == 0) loads[2 * nl] = -1;
+}
+
+// seed_resident (cache.py:197-204): append to T1 without ARC bookkeeping.
+__global__ void arc_seed_kernel(EngineDev d, int layer, const int32_t *experts, int n, int32_t *loads) {
+  if (threadIdx.x) return;
+  ArcLayer &a = d.arc[layer];
+  int nl = 0;
+  for (int i = 0; i < n; ++i) {
+    if (a.n1 + a.n2 >= a.c) break;
+    const int e = experts[i];
+    if (d.buf_of[layer * d.E + e] >= 0) continue;
+    a.t1[a.n1++] = e;
+    const int b = pop_free(d);
+    d.buf_bits[b] = d.cached_bits;
+    d.buf_of[layer * d.E + e] = b;
+    loads[2 * nl] = e;
+    loads[2 * nl + 1] = b;
+    ++nl;
+  }
+  loads[2 * nl] = -1;
+}
+
+__global__ void engine_reset_kernel(EngineDev d, const int32_t *caps) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nth = gridDim.x * blockDim.x;
+  for (int i = tid; i < d.L * d.E; i += nth) {
+    d.buf_of[i] = -1;
+    d.pend_buf[i] = -1;
+    d.pend_gen[i] = 0;
+  }
+  for (int i = tid; i < d.nbuf; i += nth) {
+    d.free_stack[i] = d.nbuf - 1 - i;
+    d.buf_gen[i] = 0;
+    d.buf_done[i] = 0xFFFFFFFFu;
+  }
+  for (int l = tid; l < d.L; l += nth) {
+    ArcLayer &a = d.arc[l];
+    a.c = caps[l];
+    a.n1 = a.n2 = a.nb1 = a.nb2 = 0;
+    a.p = 0.0;
+  }
+  if (tid == 0) {
+    Ctrl &C = *d.ctrl;
+    C.free_top = d.nbuf;
+    C.err = 0;
+    C.arrive = 0;
+    C.prev_valid = 0;
+    C.pred_valid = 0;
+    C.next_token = 0;
+    C.step = 0;
+  }
+}
+
+__global__ void run_begin_kernel(EngineDev d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    Ctrl &C = *d.ctrl;
+    C.next_token = 0;
+    C.step = 0;
+    C.arrive = 0;
+    C.prev_valid = 0;
+    C.pred_valid = 0;
+    C.err = 0;
+    // pending prefetches never outlive a run
+    for (int i = 0; i < d.L * d.E; ++i) {
+      if (d.pend_buf[i] >= 0) push_free(d, d.pend_buf[i]);
+      d.pend_buf[i] = -1;
+    }
+    *d.stats = DevStats{};
+  }
+}
+
+}  // namespace
+}  // namespace fate
+
+using namespace fate;
+
+// ---------------------------------------------------------------------------
+// Host side
+
+struct Transfer {
+  int kind;  // 0 prefetch, 1 ondemand, 2 signal-only
+  int step, layer, expert, bits, buf;
+  uint32_t gen;
+  int signal_token;   // >= 0: write ready[layer] = signal_token + 1 after this copy
+  int signal_layer;
+};
+
+struct Inflight {
+  uint32_t seq;
+  Transfer t;
+  int ev;  // index of the start/stop event pair (-1 untimed)
+};
+
+struct fate_engine {
+  fate_engine_config cfg{};
+  std::vector<int32_t> caps;
+  EngineDev d{};
+  int64_t buf_stride = 0;
+  // device allocations
+  void *dev_block = nullptr;
+  uint8_t *pool = nullptr;
+  int32_t *caps_dev = nullptr;
+  int32_t *scratch_i = nullptr;  // small scratch for standalone calls
+  float *a_scratch = nullptr;
+  // mapped pinned host memory
+  StepMsg *ring_host = nullptr;
+  volatile uint32_t *ready_host = nullptr;     // [L]
+  uint32_t *ready_dev = nullptr;
+  volatile uint32_t *copy_done_host = nullptr;
+  CUdeviceptr copy_done_dev = 0;
+  // host pools
+  const uint8_t *host_pool[17] = {};
+  int64_t host_stride[17] = {};
+  std::vector<const uint8_t *> shared_dev;
+  const uint8_t **shared_table_dev = nullptr;
+  cudaStream_t cstream = nullptr, xstream = nullptr;
+  int max_total_I = 0;
+  int prefill_max_tokens = 0;
+  // prefill scratch
+  void *pf_block = nullptr;
+  std::mutex mu;
+  // last run's timeline (ms from the run's first event)
+  std::vector<double> step_ms;     // [steps][4]: gate start/end, moe start/end
+  std::vector<double> copy_ms;     // [copies][2]
+  std::vector<int32_t> copy_meta;  // [copies][5]: kind, step, layer, expert, bits
+};
+
+namespace {
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+int check_cfg(const fate_engine_config *c) {
+  if (!c || c->num_layers < 1 || c->num_experts < 1 || c->num_experts > FATE_MAX_EXPERTS || c->top_k < 1 ||
+      c->top_k > c->num_experts || c->top_k > FATE_MAX_TOPK || c->hidden_dim < 64 || c->hidden_dim % 64 ||
+      c->intermediate_dim < 64 || c->intermediate_dim % 64 || c->shared_intermediate < 0 ||
+      c->shared_intermediate % 64 || !c->capacity || c->budget_n < 0 || c->max_tokens < 1) {
+    set_error("fate_engine_create: invalid geometry");
+    return FATE_EINVAL;
+  }
+  auto okb = [](int b) { return b == 2 || b == 4 || b == 8 || b == 16; };
+  if (!okb(c->prefetch_bits) || !okb(c->ondemand_bits) || !okb(c->cached_bits) ||
+      (c->shared_intermediate && !okb(c->shared_bits)) || !okb(c->prefill_ondemand_bits)) {
+    set_error("fate_engine_create: bit widths must be 2, 4, 8 or 16");
+    return FATE_EINVAL;
+  }
+  if (c->policy != 0 && c->policy != 1) {
+    set_error("fate_engine_create: policy must be 0 (topk) or 1 (percentile)");
+    return FATE_EINVAL;
+  }
+  for (int l = 0; l < c->num_layers; ++l)
+    if (c->capacity[l] < 0 || c->capacity[l] > c->num_experts) {
+      set_error("fate_engine_create: capacity must lie in [0, num_experts]");
+      return FATE_EINVAL;
+    }
+  return FATE_OK;
+}
+
+int copy_to_buffers(fate_engine *g, const int32_t *loads_dev, int layer, int bits) {
+  // loads: pairs (expert, buffer) terminated by -1; -2 marks a skipped entry
+  std::vector<int32_t> h(2 * FATE_MAX_EXPERTS + 2);
+  FATE_CUDA(cudaMemcpy(h.data(), loads_dev, h.size() * 4, cudaMemcpyDeviceToHost));
+  if (!g->host_pool[bits]) {
+    set_error("no pinned host pool registered for the cached bit width");
+    return FATE_EINVAL;
+  }
+  const int64_t bytes = buffer_bytes(g->cfg.hidden_dim, g->cfg.intermediate_dim, bits);
+  for (int i = 0; h[2 * i] != -1; ++i) {
+    if (h[2 * i] < 0) continue;
+    const uint8_t *src = g->host_pool[bits] + ((int64_t)layer * g->cfg.num_experts + h[2 * i]) * g->host_stride[bits];
+    FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)h[2 * i + 1] * g->buf_stride, src, bytes, cudaMemcpyHostToDevice,
+                              g->xstream));
+  }
+  FATE_CUDA(cudaStreamSynchronize(g->xstream));
+  return FATE_OK;
+}
+
+}  // namespace
+
+extern "C" int fate_version(void) { return 1; }
+extern "C" const char *fate_last_error(void) { return g_err.c_str(); }
+
+extern "C" int fate_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return cuda_status(e, "cudaGetDeviceCount");
+  }
+  *count = n;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **out) {
+  if (int st = check_cfg(cfg)) return st;
+  *out = nullptr;
+  if (int st = resolve_driver()) return st;
+  fate_engine *g = new fate_engine();
+  g->cfg = *cfg;
+  g->caps.assign(cfg->capacity, cfg->capacity + cfg->num_layers);
+  g->cfg.capacity = g->caps.data();
+  if (g->cfg.max_inflight < 1) g->cfg.max_inflight = 2;
+  FATE_CUDA(cudaSetDevice(cfg->device));
+  const int L = cfg->num_layers, E = cfg->num_experts, k = cfg->top_k, H = cfg->hidden_dim, I = cfg->intermediate_dim;
+  int S = 0;
+  for (int c : g->caps) S += c;
+  // staging: prefetches for l and l+1 in flight plus the step's on-demand loads
+  const int n_max = E;  // any later set_strategy may raise n up to E
+  const int staging_decode = 2 * n_max + 2 * k + 4;
+  const int staging_prefill = 2 * E + 4;
+  const int nbuf = S + std::max(staging_decode, staging_prefill);
+  int64_t bb = 0;
+  for (int b : {cfg->prefetch_bits, cfg->ondemand_bits, cfg->cached_bits, cfg->prefill_ondemand_bits, 4, 2})
+    bb = std::max<int64_t>(bb, buffer_bytes(H, I, b));
+  g->buf_stride = align_up(bb, 4096);
+  EngineDev &d = g->d;
+  d.L = L, d.E = E, d.k = k, d.H = H, d.I = I;
+  d.I_shared = cfg->shared_intermediate;
+  d.shared_bits = cfg->shared_bits;
+  d.cached_bits = cfg->cached_bits;
+  d.prefetch_bits = cfg->prefetch_bits;
+  d.ondemand_bits = cfg->ondemand_bits;
+  d.use_predictor = cfg->use_predictor;
+  d.policy = cfg->policy;
+  d.budget_n = std::min(cfg->budget_n, E);
+  g->cfg.budget_n = d.budget_n;
+  d.q = cfg->percentile_q;
+  d.nbuf = nbuf;
+  d.buf_stride = g->buf_stride;
+  g->max_total_I = k * I + cfg->shared_intermediate;
+  // one block for the small device state
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = off;
+    off = (size_t)align_up((int64_t)(off + bytes), 256);
+    return o;
+  };
+  const size_t o_W = carve((size_t)L * E * H * 8), o_tau = carve((size_t)L * 8), o_arc = carve((size_t)L * sizeof(ArcLayer)),
+               o_bof = carve((size_t)L * E * 4), o_pb = carve((size_t)L * E * 4), o_pg = carve((size_t)L * E * 4),
+               o_fs = carve((size_t)nbuf * 4), o_bg = carve((size_t)nbuf * 4), o_bd = carve((size_t)nbuf * 4),
+               o_bb = carve((size_t)nbuf * 4),
+               o_ctrl = carve(sizeof(Ctrl)), o_st = carve(sizeof(DevStats)), o_lg = carve(2 * EMAX * 8),
+               o_x = carve((size_t)std::max(H, 4096) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
+               o_sh = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
+               o_a = carve((size_t)g->max_total_I * 4);
+  FATE_CUDA(cudaMalloc(&g->dev_block, off));
+  FATE_CUDA(cudaMemset(g->dev_block, 0, off));
+  uint8_t *base = (uint8_t *)g->dev_block;
+  d.W = (const double *)(base + o_W);
+  d.tau = (const double *)(base + o_tau);
+  d.arc = (ArcLayer *)(base + o_arc);
+  d.buf_of = (int32_t *)(base + o_bof);
+  d.pend_buf = (int32_t *)(base + o_pb);
+  d.pend_gen = (uint32_t *)(base + o_pg);
+  d.free_stack = (int32_t *)(base + o_fs);
+  d.buf_gen = (uint32_t *)(base + o_bg);
+  d.buf_done = (uint32_t *)(base + o_bd);
+  d.buf_bits = (int32_t *)(base + o_bb);
+  d.ctrl = (Ctrl *)(base + o_ctrl);
+  d.stats = (DevStats *)(base + o_st);
+  d.logits = (double *)(base + o_lg);
+  d.x = (float *)(base + o_x);
+  d.batch = (FfnBatch *)(base + o_b);
+  g->caps_dev = (int32_t *)(base + o_caps);
+  g->shared_table_dev = (const uint8_t **)(base + o_sh);
+  d.shared = cfg->shared_intermediate ? g->shared_table_dev : nullptr;
+  g->scratch_i = (int32_t *)(base + o_si);
+  g->a_scratch = (float *)(base + o_a);
+  FATE_CUDA(cudaMalloc(&g->pool, (size_t)nbuf * g->buf_stride));
+  d.pool = g->pool;
+  FATE_CUDA(cudaMemcpy(g->caps_dev, g->caps.data(), L * 4, cudaMemcpyHostToDevice));
+  g->shared_dev.assign(L, nullptr);
+  // mapped pinned host memory: mailbox ring, ready flags, copy counter
+  void *p = nullptr;
+  FATE_CUDA(cudaHostAlloc(&p, sizeof(StepMsg) * kRing, cudaHostAllocMapped));
+  memset(p, 0, sizeof(StepMsg) * kRing);
+  g->ring_host = (StepMsg *)p;
+  void *pd = nullptr;
+  FATE_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
+  d.ring = (StepMsg *)pd;
+  FATE_CUDA(cudaHostAlloc(&p, 4096, cudaHostAllocMapped));
+  memset(p, 0, 4096);
+  g->ready_host = (volatile uint32_t *)p;
+  g->copy_done_host = (volatile uint32_t *)((uint8_t *)p + 2048);
+  FATE_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
+  g->ready_dev = (uint32_t *)pd;
+  g->copy_done_dev = (CUdeviceptr)((uint8_t *)pd + 2048);
+  int lo = 0, hi = 0;
+  FATE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  FATE_CUDA(cudaStreamCreateWithPriority(&g->cstream, cudaStreamNonBlocking, hi));
+  FATE_CUDA(cudaStreamCreateWithPriority(&g->xstream, cudaStreamNonBlocking, lo));
+  // load every kernel the engine launches now: lazy module loading at first
+  // launch can deadlock behind a stream parked on a cuStreamWaitValue32 flag
+  {
+    cudaFuncAttributes fa;
+    FATE_CUDA(cudaFuncGetAttributes(&fa, decode_gate_kernel));
+    FATE_CUDA(cudaFuncGetAttributes(&fa, arc_flush_kernel));
+    FATE_CUDA(cudaFuncGetAttributes(&fa, arc_access_kernel));
+    FATE_CUDA(cudaFuncGetAttributes(&fa, arc_seed_kernel));
+    FATE_CUDA(cudaFuncGetAttributes(&fa, run_begin_kernel));
+    FATE_CUDA(ffn_preload());
+  }
+  engine_reset_kernel<<<64, 256, 0, g->cstream>>>(d, g->caps_dev);
+  FATE_CHECK_LAUNCH("engine_reset_kernel");
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  *out = g;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_destroy(fate_engine *g) {
+  if (!g) return FATE_OK;
+  cudaStreamSynchronize(g->cstream);
+  cudaStreamSynchronize(g->xstream);
+  cudaStreamDestroy(g->cstream);
+  cudaStreamDestroy(g->xstream);
+  cudaFree(g->pool);
+  cudaFree(g->dev_block);
+  if (g->pf_block) cudaFree(g->pf_block);
+  cudaFreeHost(g->ring_host);
+  cudaFreeHost((void *)g->ready_host);
+  delete g;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_gate(fate_engine *g, const double *W_host, const double *tau_host) {
+  const size_t n = (size_t)g->cfg.num_layers * g->cfg.num_experts * g->cfg.hidden_dim;
+  FATE_CUDA(cudaMemcpy((void *)g->d.W, W_host, n * 8, cudaMemcpyHostToDevice));
+  FATE_CUDA(cudaMemcpy((void *)g->d.tau, tau_host, g->cfg.num_layers * 8, cudaMemcpyHostToDevice));
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_host_pool(fate_engine *g, int bits, const uint8_t *base, int64_t stride) {
+  if (!(bits == 2 || bits == 4 || bits == 8 || bits == 16) ||
+      stride < buffer_bytes(g->cfg.hidden_dim, g->cfg.intermediate_dim, bits)) {
+    set_error("fate_engine_set_host_pool: bad bits or stride");
+    return FATE_EINVAL;
+  }
+  g->host_pool[bits] = base;
+  g->host_stride[bits] = stride;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_shared(fate_engine *g, int layer, const uint8_t *buf_dev) {
+  if (layer < 0 || layer >= g->cfg.num_layers || !g->cfg.shared_intermediate) {
+    set_error("fate_engine_set_shared: bad layer or engine has no shared expert");
+    return FATE_EINVAL;
+  }
+  g->shared_dev[layer] = buf_dev;
+  FATE_CUDA(cudaMemcpy(g->shared_table_dev, g->shared_dev.data(), g->cfg.num_layers * sizeof(void *),
+                       cudaMemcpyHostToDevice));
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_reset_cache(fate_engine *g) {
+  engine_reset_kernel<<<64, 256, 0, g->cstream>>>(g->d, g->caps_dev);
+  FATE_CHECK_LAUNCH("engine_reset_kernel");
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_seed_resident(fate_engine *g, int layer, const int32_t *experts, int n) {
+  if (layer < 0 || layer >= g->cfg.num_layers || n < 0 || n > FATE_MAX_EXPERTS) {
+    set_error("fate_engine_seed_resident: bad arguments");
+    return FATE_EINVAL;
+  }
+  int32_t *ex = g->scratch_i, *loads = g->scratch_i + FATE_MAX_EXPERTS;
+  FATE_CUDA(cudaMemcpy(ex, experts, n * 4, cudaMemcpyHostToDevice));
+  arc_seed_kernel<<<1, 32, 0, g->cstream>>>(g->d, layer, ex, n, loads);
+  FATE_CHECK_LAUNCH("arc_seed_kernel");
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  return copy_to_buffers(g, loads, layer, g->cfg.cached_bits);
+}
+
+extern "C" int fate_engine_resident(fate_engine *g, int layer, int32_t *out) {
+  if (layer < 0 || layer >= g->cfg.num_layers) {
+    set_error("fate_engine_resident: bad layer");
+    return FATE_EINVAL;
+  }
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  std::vector<int32_t> h(g->cfg.num_experts);
+  FATE_CUDA(cudaMemcpy(h.data(), g->d.buf_of + layer * g->cfg.num_experts, h.size() * 4, cudaMemcpyDeviceToHost));
+  for (int e = 0; e < g->cfg.num_experts; ++e) out[e] = h[e] >= 0;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_access(fate_engine *g, int layer, const int32_t *experts, int n, int32_t *hits) {
+  if (layer < 0 || layer >= g->cfg.num_layers || n < 0 || n > FATE_MAX_EXPERTS) {
+    set_error("fate_engine_access: bad arguments");
+    return FATE_EINVAL;
+  }
+  for (int i = 0; i < n; ++i)
+    if (experts[i] < 0 || experts[i] >= g->cfg.num_experts) {
+      set_error("fate_engine_access: expert id out of range");
+      return FATE_EINVAL;
+    }
+  int32_t *ex = g->scratch_i, *loads = g->scratch_i + FATE_MAX_EXPERTS + 1;
+  int32_t *hits_dev = g->scratch_i + 3 * FATE_MAX_EXPERTS + 3;
+  if (n == 0) return FATE_OK;
+  FATE_CUDA(cudaMemcpy(ex, experts, n * 4, cudaMemcpyHostToDevice));
+  arc_access_kernel<<<1, 32, 0, g->cstream>>>(g->d, layer, ex, n, hits_dev, loads);
+  FATE_CHECK_LAUNCH("arc_access_kernel");
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  FATE_CUDA(cudaMemcpy(hits, hits_dev, n * 4, cudaMemcpyDeviceToHost));
+  return copy_to_buffers(g, loads, layer, g->cfg.cached_bits);
+}
+
+extern "C" int fate_engine_arc_state(fate_engine *g, int layer, int32_t *t1, int32_t *t2, int32_t *b1, int32_t *b2,
+                                     int32_t *lens, double *p) {
+  if (layer < 0 || layer >= g->cfg.num_layers) {
+    set_error("fate_engine_arc_state: bad layer");
+    return FATE_EINVAL;
+  }
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  ArcLayer a;
+  FATE_CUDA(cudaMemcpy(&a, g->d.arc + layer, sizeof(a), cudaMemcpyDeviceToHost));
+  const int E = g->cfg.num_experts;
+  memcpy(t1, a.t1, std::min(a.n1, E) * 4);
+  memcpy(t2, a.t2, std::min(a.n2, E) * 4);
+  memcpy(b1, a.b1, std::min(a.nb1, E) * 4);
+  memcpy(b2, a.b2, std::min(a.nb2, E) * 4);
+  lens[0] = a.n1, lens[1] = a.n2, lens[2] = a.nb1, lens[3] = a.nb2;
+  *p = a.p;
+  return FATE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The transfer channel on the host (pipeline.py:163-264 semantics).
+
+namespace {
+
+struct Channel {
+  fate_engine *g;
+  std::deque<Transfer> pending;
+  std::deque<Inflight> inflight;
+  uint32_t submitted = 0;
+  int64_t h2d_bytes = 0, done = 0, dropped = 0;
+  bool timed = false;
+  cudaEvent_t t0 = nullptr;      // run start, for absolute copy timestamps
+  std::vector<cudaEvent_t> ev;  // pairs, recycled through ev_free once reaped
+  std::vector<int> ev_free;
+  double copy_ms = 0.0;
+
+  int bytes_of(int bits) const { return (int)buffer_bytes(g->cfg.hidden_dim, g->cfg.intermediate_dim, bits); }
+
+  int submit_one(const Transfer &t) {
+    const cudaStream_t s = g->xstream;
+    int evi = -1;
+    if (t.kind != 2) {
+      if (!g->host_pool[t.bits]) {
+        set_error("no pinned host pool registered for a requested bit width");
+        return FATE_EINVAL;
+      }
+      const int64_t bytes = bytes_of(t.bits);
+      const uint8_t *src = g->host_pool[t.bits] + ((int64_t)t.layer * g->cfg.num_experts + t.expert) * g->host_stride[t.bits];
+      if (timed && !ev_free.empty()) {
+        evi = ev_free.back();
+        ev_free.pop_back();
+        FATE_CUDA(cudaEventRecord(ev[evi], s));
+      }
+      FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)t.buf * g->buf_stride, src, bytes, cudaMemcpyHostToDevice, s));
+      if (evi >= 0) FATE_CUDA(cudaEventRecord(ev[evi + 1], s));
+      FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
+      h2d_bytes += bytes;
+    }
+    ++submitted;
+    FATE_CU(p_write32((CUstream)s, g->copy_done_dev, submitted, 0));
+    inflight.push_back(Inflight{submitted, t, evi});
+    return FATE_OK;
+  }
+
+  void reap() {
+    const uint32_t c = *g->copy_done_host;
+    while (!inflight.empty() && (int32_t)(c - inflight.front().seq) >= 0) {
+      Inflight &f = inflight.front();
+      if (f.ev >= 0) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev[f.ev], ev[f.ev + 1]) == cudaSuccess) copy_ms += ms;
+        float a = 0.f, b = 0.f;
+        if (t0 && cudaEventElapsedTime(&a, t0, ev[f.ev]) == cudaSuccess &&
+            cudaEventElapsedTime(&b, t0, ev[f.ev + 1]) == cudaSuccess) {
+          g->copy_ms.push_back(a);
+          g->copy_ms.push_back(b);
+          const int32_t meta[5] = {f.t.kind, f.t.step, f.t.layer, f.t.expert, f.t.bits};
+          g->copy_meta.insert(g->copy_meta.end(), meta, meta + 5);
+        }
+        ev_free.push_back(f.ev);
+      }
+      if (f.t.kind != 2) ++done;
+      if (f.t.signal_token >= 0) g->ready_host[f.t.signal_layer] = (uint32_t)f.t.signal_token + 1u;
+      inflight.pop_front();
+    }
+  }
+
+  int pump() {
+    reap();
+    while ((int)inflight.size() < g->cfg.max_inflight && !pending.empty()) {
+      Transfer t = pending.front();
+      pending.pop_front();
+      if (int st = submit_one(t)) return st;
+    }
+    return FATE_OK;
+  }
+
+  // promote_ondemand (pipeline.py:241-245): stable partition, on-demand first
+  void promote() {
+    std::stable_partition(pending.begin(), pending.end(), [](const Transfer &t) { return t.kind != 0; });
+  }
+};
+
+}  // namespace
+
+extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, const int32_t *chosen_dev, int T,
+                                  float *y_dev, fate_step_log *log_dev, fate_run_stats *stats) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  const int L = g->cfg.num_layers, H = g->cfg.hidden_dim;
+  if (T < 0 || T > g->cfg.max_tokens) {
+    set_error("fate_engine_decode: T exceeds max_tokens");
+    return FATE_EINVAL;
+  }
+  fate_run_stats st{};
+  if (T == 0) {
+    if (stats) *stats = st;
+    return FATE_OK;
+  }
+  if (!g->host_pool[g->cfg.ondemand_bits] || (g->cfg.use_predictor && !g->host_pool[g->cfg.prefetch_bits])) {
+    set_error("fate_engine_decode: pinned host pool missing for the strategy's bit widths");
+    return FATE_EINVAL;
+  }
+  if (g->cfg.shared_intermediate)
+    for (int l = 0; l < L; ++l)
+      if (!g->shared_dev[l]) {
+        set_error("fate_engine_decode: shared expert buffer missing");
+        return FATE_EINVAL;
+      }
+  cudaSetDevice(g->cfg.device);
+  const bool timed = stats != nullptr;
+  const int n_steps = T * L;
+  Channel ch;
+  ch.g = g;
+  ch.timed = timed;
+  std::vector<cudaEvent_t> kev;  // per step: K1 start, K1 end, K3 start (after the wait), K3 end
+  if (timed) {
+    ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
+    for (auto &e : ch.ev) FATE_CUDA(cudaEventCreate(&e));
+    for (int i = (int)ch.ev.size() - 2; i >= 0; i -= 2) ch.ev_free.push_back(i);
+    kev.resize(4 * (size_t)n_steps);
+    for (auto &e : kev) FATE_CUDA(cudaEventCreate(&e));
+    ch.t0 = kev[0];
+  }
+  g->step_ms.clear();
+  g->copy_ms.clear();
+  g->copy_meta.clear();
+  for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
+  *g->copy_done_host = 0;
+  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
+  const cudaStream_t cs = g->cstream;
+  if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
+  run_begin_kernel<<<1, 1, 0, cs>>>(g->d);
+  FATE_CHECK_LAUNCH("run_begin_kernel");
+  FATE_CUDA(cudaStreamSynchronize(cs));
+  if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] run_begin done\n");
+  int launched = 0, processed = 0;
+  const int lookahead = 4;
+  int status = FATE_OK;
+  auto last_progress = std::chrono::steady_clock::now();
+  const int rows_pred = g->cfg.use_predictor ? 2 : 1;
+  const bool dbg = getenv("FATE_DEBUG") != nullptr;
+  auto last_beat = std::chrono::steady_clock::now();
+  while (processed < n_steps) {
+    if (dbg && std::chrono::steady_clock::now() - last_beat > std::chrono::seconds(2)) {
+      last_beat = std::chrono::steady_clock::now();
+      fprintf(stderr, "[fate] beat processed=%d launched=%d pending=%zu inflight=%zu submitted=%u copy_done=%u seq=%u\n",
+              processed, launched, ch.pending.size(), ch.inflight.size(), ch.submitted, *g->copy_done_host,
+              g->ring_host[processed % kRing].seq);
+    }
+    // enqueue compute for steps up to `lookahead` beyond the host's progress
+    while (launched < n_steps && launched < processed + lookahead) {
+      const int s = launched, t = s / L, l = s % L;
+      const int rows = (rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts;
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
+      decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
+                                                        (volatile uint32_t *)g->ready_dev);
+      FATE_CHECK_LAUNCH("decode_gate_kernel");
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
+      if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
+      FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
+                                  CU_STREAM_WAIT_VALUE_GEQ));
+      if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+      FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                         g->max_total_I, &g->d.stats->ffn_bytes, cs));
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+      if (dbg && s < 2) fprintf(stderr, "[fate] launched K3 step %d\n", s);
+      ++launched;
+    }
+    // service the step message of the next unprocessed step
+    StepMsg &m = g->ring_host[processed % kRing];
+    if (m.seq == (uint32_t)processed + 1u) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      const int t = m.token, l = m.layer;
+      // drop queued prefetches for this step that the gate did not choose
+      for (int i = 0; i < m.n_drop; ++i) {
+        const int e = m.drop_e[i];
+        auto it = std::find_if(ch.pending.begin(), ch.pending.end(), [&](const Transfer &x) {
+          return x.kind == 0 && x.layer == l && x.expert == e && x.step == t;
+        });
+        if (it != ch.pending.end()) {
+          ch.pending.erase(it);
+          ++ch.dropped;
+        }
+      }
+      // prefetches for layer l+1 (issued at gate start, pipeline.py:414-417)
+      for (int i = 0; i < m.n_pf; ++i)
+        ch.pending.push_back(Transfer{0, t, l + 1, m.pf_e[i], m.pf_bits_each[i], m.pf_b[i], m.pf_g[i], -1, -1});
+      // on-demand loads for this step, promoted ahead of every prefetch
+      for (int i = 0; i < m.n_od; ++i)
+        ch.pending.push_back(Transfer{1, t, l, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
+      ch.promote();
+      if (!m.self_signaled) {
+        // the compute stream may proceed once every needed transfer landed:
+        // attach the signal to the last needed one still queued, else signal
+        // behind everything already submitted.
+        int last = -1;
+        for (int i = 0; i < (int)ch.pending.size(); ++i) {
+          const Transfer &x = ch.pending[i];
+          bool need = x.kind == 1 && x.layer == l && x.step == t;
+          for (int j = 0; !need && j < m.n_need; ++j) need = x.kind == 0 && x.layer == l && x.expert == m.need_e[j];
+          if (need) last = i;
+        }
+        if (last >= 0) {
+          ch.pending[last].signal_token = t;
+          ch.pending[last].signal_layer = l;
+        } else {
+          ch.pending.push_front(Transfer{2, t, l, -1, 0, -1, 0, t, l});
+        }
+      }
+      if (dbg)
+        fprintf(stderr, "[fate] msg step=%d t=%d l=%d self=%d od=%d need=%d drop=%d pf=%d pending=%zu inflight=%zu\n",
+                processed, t, l, m.self_signaled, m.n_od, m.n_need, m.n_drop, m.n_pf, ch.pending.size(),
+                ch.inflight.size());
+      ++processed;
+      last_progress = std::chrono::steady_clock::now();
+    }
+    if ((status = ch.pump())) break;
+    if (m.seq != (uint32_t)processed + 1u) {
+      _mm_pause();
+      if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(30)) {
+        // watchdog: release the compute stream so the GPU is never left hung
+        for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
+        status = FATE_ETIMEOUT;
+        set_error("fate_engine_decode: no progress for 30 s (copy or kernel stalled)");
+        break;
+      }
+    }
+  }
+  if (status != FATE_OK) {
+    // never leave the compute stream parked on a flag nobody will write
+    for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+  }
+  if (getenv("FATE_DEBUG"))
+    fprintf(stderr, "[fate] decode loop exit status=%d processed=%d/%d pending=%zu inflight=%zu err=%s\n", status,
+            processed, n_steps, ch.pending.size(), ch.inflight.size(), g_err.c_str());
+  // drain remaining copies (stale prefetches for a layer past the end)
+  while (status == FATE_OK && (!ch.pending.empty() || !ch.inflight.empty())) {
+    // every message has been processed: whatever is still queued was needed by
+    // some step (unneeded prefetches were dropped at their step), so finish it
+    if ((status = ch.pump())) break;
+    _mm_pause();
+    if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(30)) {
+      status = FATE_ETIMEOUT;
+      set_error("fate_engine_decode: copies never completed while draining");
+      for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
+      break;
+    }
+  }
+  arc_flush_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
+  cudaError_t fe = cudaGetLastError();
+  cudaError_t se = cudaStreamSynchronize(cs);
+  cudaError_t xe = cudaStreamSynchronize(g->xstream);
+  if (status == FATE_OK && fe != cudaSuccess) status = cuda_status(fe, "arc_flush_kernel");
+  if (status == FATE_OK && se != cudaSuccess) status = cuda_status(se, "decode compute stream");
+  if (status == FATE_OK && xe != cudaSuccess) status = cuda_status(xe, "decode copy stream");
+  DevStats ds{};
+  Ctrl cc{};
+  if (status == FATE_OK) {
+    FATE_CUDA(cudaMemcpy(&ds, g->d.stats, sizeof(ds), cudaMemcpyDeviceToHost));
+    FATE_CUDA(cudaMemcpy(&cc, g->d.ctrl, sizeof(cc), cudaMemcpyDeviceToHost));
+    if (cc.err) {
+      set_error("fate_engine_decode: staging buffer pool exhausted");
+      status = FATE_ENOMEM;
+    }
+  }
+  if (timed && status == FATE_OK) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, kev[0], kev[4 * (n_steps - 1) + 3]);
+    st.gpu_ms = ms;
+    double ffn = 0.0, gate = 0.0;
+    g->step_ms.resize(4 * (size_t)n_steps);
+    for (int s = 0; s < n_steps; ++s) {
+      float t[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 1; j < 4; ++j) cudaEventElapsedTime(&t[j], kev[0], kev[4 * s + j]);
+      if (s) cudaEventElapsedTime(&t[0], kev[0], kev[4 * s]);
+      for (int j = 0; j < 4; ++j) g->step_ms[4 * (size_t)s + j] = t[j];
+      gate += t[1] - t[0];
+      ffn += t[3] - t[2];
+    }
+    st.ffn_ms = ffn;
+    st.gate_ms = gate;
+  }
+  if (timed) {
+    for (auto &e : ch.ev) cudaEventDestroy(e);
+    for (auto &e : kev) cudaEventDestroy(e);
+  }
+  st.steps = n_steps;
+  st.accesses = (int64_t)ds.accesses;
+  st.cache_hits = (int64_t)ds.cache_hits;
+  st.arrival_hits = (int64_t)ds.arrival_hits;
+  st.dequant_count = (int64_t)ds.dequant_count;
+  st.prefetch_issued = (int64_t)ds.prefetch_issued;
+  st.ondemand_issued = (int64_t)ds.ondemand_issued;
+  st.transfers_done = ch.done;
+  st.transfers_dropped = ch.dropped;
+  st.h2d_bytes = ch.h2d_bytes;
+  st.copy_busy_ms = ch.copy_ms;
+  st.recall_sum = ds.recall_sum;
+  st.recall_n = (int64_t)ds.recall_n;
+  st.trace_mismatches = (int64_t)ds.mismatches;
+  st.near_ties = (int64_t)ds.near_ties;
+  st.ffn_bytes = (int64_t)ds.ffn_bytes;
+  st.error = status;
+  if (stats) *stats = st;
+  return status;
+}
+
+extern "C" int fate_engine_timeline(fate_engine *g, double *step_ms, int max_steps, double *copy_ms, int32_t *copy_meta,
+                                    int max_copies, int32_t *counts) {
+  const int ns = (int)(g->step_ms.size() / 4), nc = (int)(g->copy_ms.size() / 2);
+  counts[0] = ns;
+  counts[1] = nc;
+  if (step_ms) memcpy(step_ms, g->step_ms.data(), sizeof(double) * 4 * std::min(ns, max_steps));
+  if (copy_ms) memcpy(copy_ms, g->copy_ms.data(), sizeof(double) * 2 * std::min(nc, max_copies));
+  if (copy_meta) memcpy(copy_meta, g->copy_meta.data(), sizeof(int32_t) * 5 * std::min(nc, max_copies));
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_strategy(fate_engine *g, const fate_engine_config *c) {
+  if (int st = check_cfg(c)) return st;
+  const int H = g->cfg.hidden_dim, I = g->cfg.intermediate_dim;
+  for (int b : {c->prefetch_bits, c->ondemand_bits, c->cached_bits, c->prefill_ondemand_bits})
+    if (buffer_bytes(H, I, b) > g->buf_stride) {
+      set_error("fate_engine_set_strategy: strategy needs wider expert buffers than the engine was built with");
+      return FATE_EINVAL;
+    }
+  g->cfg.cached_bits = c->cached_bits;
+  g->cfg.prefetch_bits = c->prefetch_bits;
+  g->cfg.ondemand_bits = c->ondemand_bits;
+  g->cfg.use_predictor = c->use_predictor;
+  g->cfg.policy = c->policy;
+  g->cfg.percentile_q = c->percentile_q;
+  g->cfg.budget_n = std::min(c->budget_n, g->cfg.num_experts);
+  g->cfg.prefill_use_predictor = c->prefill_use_predictor;
+  g->cfg.reorder_prefill = c->reorder_prefill;
+  g->cfg.p_int2 = c->p_int2;
+  g->cfg.prefill_ondemand_bits = c->prefill_ondemand_bits;
+  if (c->max_inflight > 0) g->cfg.max_inflight = c->max_inflight;
+  EngineDev &d = g->d;
+  d.cached_bits = c->cached_bits;
+  d.prefetch_bits = c->prefetch_bits;
+  d.ondemand_bits = c->ondemand_bits;
+  d.use_predictor = c->use_predictor;
+  d.policy = c->policy;
+  d.q = c->percentile_q;
+  d.budget_n = g->cfg.budget_n;
+  return FATE_OK;
+}

@@ -1,0 +1,90 @@
+// Device-side state of the offload engine: ARC tables, expert->buffer maps,
+// the staging free stack, the step control block and the host mailbox.
+#pragma once
+
+#include "fate_internal.cuh"
+
+namespace fate {
+
+constexpr int EMAX = FATE_MAX_EXPERTS;
+constexpr int KMAX = FATE_MAX_TOPK;
+
+// One layer's ARC lists (cache.py:104-179), LRU first.
+struct ArcLayer {
+  int32_t c, n1, n2, nb1, nb2, pad0;
+  double p;
+  int32_t t1[EMAX], t2[EMAX], b1[EMAX], b2[EMAX];
+};
+
+// Step message, device -> host (mapped pinned memory).  `seq` is written last.
+struct StepMsg {
+  volatile uint32_t seq;
+  int32_t step, token, layer;
+  int32_t self_signaled;
+  int32_t n_od, n_need, n_drop, n_pf;
+  int32_t od_bits, pf_bits;
+  int32_t od_e[EMAX], od_b[EMAX];
+  uint32_t od_g[EMAX];
+  int32_t need_e[EMAX], need_b[EMAX];
+  int32_t drop_e[EMAX], drop_b[EMAX];
+  int32_t pf_e[EMAX], pf_b[EMAX], pf_bits_each[EMAX];
+  uint32_t pf_g[EMAX];
+  // prefill extras (host-side log + ordering)
+  int32_t n_active, n_res;
+  int32_t active_e[EMAX], active_cnt[EMAX], res_e[EMAX];
+  int32_t pred_order[EMAX], pred_cnt[EMAX], n_pred;
+  int32_t mismatch;
+};
+
+constexpr int kRing = 64;
+
+// Control block for the step sequence.
+struct Ctrl {
+  int32_t next_token;
+  int32_t cur_token, cur_layer;
+  int32_t prev_valid, prev_layer, prev_k, prev_step;
+  int32_t prev_chosen[EMAX], prev_buf[EMAX];
+  int32_t free_top;
+  int32_t err;
+  uint32_t arrive;        // K1 last-block detector
+  int32_t pred_valid, pred_layer, pred_n;
+  int32_t pred_list[EMAX];
+  int32_t step;           // global step counter (token*L + layer)
+};
+
+struct DevStats {
+  unsigned long long accesses, cache_hits, arrival_hits, dequant_count, prefetch_issued, ondemand_issued;
+  unsigned long long mismatches, near_ties, recall_n, ffn_bytes;
+  double recall_sum;
+};
+
+// All device pointers of an engine, passed to kernels by value.
+struct EngineDev {
+  int L, E, k, H, I, I_shared, shared_bits;
+  int cached_bits, prefetch_bits, ondemand_bits;
+  int use_predictor, policy, budget_n;
+  double q;
+  int nbuf;
+  int64_t buf_stride;
+  uint8_t *pool;              // nbuf * buf_stride
+  const uint8_t **shared;     // [L] shared-expert buffers (or null)
+  const double *W;            // [L, E, H]
+  const double *tau;          // [L]
+  ArcLayer *arc;              // [L]
+  int32_t *buf_of;            // [L, E]
+  int32_t *pend_buf;          // [L, E]
+  uint32_t *pend_gen;         // [L, E]
+  int32_t *free_stack;        // [nbuf]
+  uint32_t *buf_gen;          // [nbuf]
+  uint32_t *buf_done;         // [nbuf]  written by the copy stream
+  int32_t *buf_bits;          // [nbuf]  storage width requested into each buffer
+  uint32_t *ready;            // [L]     wait flags of the compute stream
+  Ctrl *ctrl;
+  DevStats *stats;
+  double *logits;             // [2E]
+  float *x;                   // [H]
+  FfnBatch *batch;
+  StepMsg *ring;              // mapped pinned [kRing]
+};
+
+}  // namespace fate

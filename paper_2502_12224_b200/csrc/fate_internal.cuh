@@ -1,0 +1,139 @@
+// Internal definitions shared by the sm_100a translation units.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fate_b200.h"
+
+namespace fate {
+
+// ---------------------------------------------------------------------------
+// Error plumbing: every C entry point returns a status and records a message.
+void set_error(const std::string &msg);
+int cuda_status(cudaError_t e, const char *what);
+
+#define FATE_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return fate::cuda_status(_e, #call); \
+  } while (0)
+
+#define FATE_CHECK_LAUNCH(what)                                         \
+  do {                                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) return fate::cuda_status(_e, what);          \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Packed expert buffer: 256-byte header followed by the payload.
+//   quantized (bits 8/4/2): codes w1 [I*H*b/8] | codes w3 | codes w2 [H*I*b/8]
+//                           | sz w1 [I*H/64 float2] | sz w3 | sz w2
+//   bf16 (bits 16):         w1 [I*H] | w3 [I*H] | w2 [H*I]
+// The payload size equals expert_bytes[bits] of quant.py:239-246.  A copy of
+// the whole buffer carries its own format, so a cache slot filled by an INT2
+// on-demand load is computed as INT2 (the "tag slot bits" decision).
+constexpr uint32_t kMagic = 0xFA7EB200u;
+constexpr int kGroup = 64;
+
+struct ExpertHeader {
+  uint32_t magic;
+  int32_t bits;
+  int32_t layer;
+  int32_t expert;
+  int32_t H;
+  int32_t I;
+  int32_t pad[58];
+};
+static_assert(sizeof(ExpertHeader) == FATE_HEADER_BYTES, "header size");
+
+struct Layout {
+  int64_t c1, c3, c2;  // code (or bf16) offsets within the payload
+  int64_t s1, s3, s2;  // float2 (scale, zero) offsets (quantized only)
+  int64_t row_bytes_up;   // bytes per row of w1/w3 (H elements)
+  int64_t row_bytes_down; // bytes per row of w2 (I elements)
+  int64_t payload;
+};
+
+__host__ __device__ inline Layout make_layout(int H, int I, int bits) {
+  Layout L{};
+  const int64_t n = (int64_t)H * I;
+  if (bits == 16) {
+    L.c1 = 0;
+    L.c3 = 2 * n;
+    L.c2 = 4 * n;
+    L.s1 = L.s3 = L.s2 = 6 * n;
+    L.row_bytes_up = 2 * (int64_t)H;
+    L.row_bytes_down = 2 * (int64_t)I;
+    L.payload = 6 * n;
+  } else {
+    const int64_t cb = n * bits / 8;
+    const int64_t sb = n / kGroup * 8;
+    L.c1 = 0;
+    L.c3 = cb;
+    L.c2 = 2 * cb;
+    L.s1 = 3 * cb;
+    L.s3 = 3 * cb + sb;
+    L.s2 = 3 * cb + 2 * sb;
+    L.row_bytes_up = (int64_t)H * bits / 8;
+    L.row_bytes_down = (int64_t)I * bits / 8;
+    L.payload = 3 * cb + 3 * sb;
+  }
+  return L;
+}
+
+inline int64_t buffer_bytes(int H, int I, int bits) {
+  return FATE_HEADER_BYTES + make_layout(H, I, bits).payload;
+}
+
+// ---------------------------------------------------------------------------
+// K3 launch interface (used both standalone and by the engine).
+struct FfnExpert {
+  const uint8_t *buf;  // packed buffer (header at buf, payload at buf + 256)
+  float weight;
+  int I;
+  int bits;
+  int a_off;           // offset of this expert's activation vector in scratch
+};
+
+constexpr int kMaxFfnExperts = FATE_MAX_TOPK + 2;
+
+struct FfnBatch {
+  int n;
+  int H;
+  int total_I;
+  FfnExpert e[kMaxFfnExperts];
+};
+
+// Launch the two K3 phases for a batch described in DEVICE memory (`batch`),
+// with upper bounds known on the host (for graph-stable grids).
+cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *x_dev, float *a_dev, float *y_dev,
+                              int H, int max_total_I, cudaStream_t s);
+
+cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *x_dev, float *a_dev, float *y_dev,
+                                     int H, int max_total_I, unsigned long long *bytes_stat, cudaStream_t s);
+
+cudaError_t ffn_preload();
+
+// K1 kernels exposed to the engine.
+cudaError_t launch_gate_batch(const double *W, double tau, const double *h, int T, int E, int H,
+                              double *routing, int32_t *order, int32_t *list_len, int top_k, int policy,
+                              double q, cudaStream_t s);
+
+// K4 grouped prefill FFN.
+struct PrefillExpert {
+  const uint8_t *buf;
+  int I;
+  int bits;
+  int tok_off;   // offset into tok_idx / tok_w
+  int n_tok;
+};
+
+cudaError_t launch_ffn_prefill(const float *X, int T, int H, int n, const PrefillExpert *experts_dev,
+                               const int32_t *tok_idx, const float *tok_w, float *Y, int max_I,
+                               int max_tok, float *scratch, cudaStream_t s);
+
+}  // namespace fate
