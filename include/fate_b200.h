@@ -67,6 +67,11 @@ int fate_quant_pack64(const double *w_dev, int64_t n, int bits, int group, uint8
 int fate_dequant(const uint8_t *codes_dev, const float *sz_dev, int64_t n, int bits, int group,
                  float *out_dev, void *stream);
 
+/* fp64 dequantization from the reference representation (fp64 scales/zeros),
+ * zero + code*scale with the reference's two roundings (quant.py:110-120). */
+int fate_dequant64(const uint8_t *codes_dev, const double *scale64_dev, const double *zero64_dev, int64_t n,
+                   int bits, int group, double *out_dev, void *stream);
+
 /* Pack one expert (w1 [I,H], w3 [I,H], w2 [H,I], fp32 on device) into the
  * engine's self-describing buffer layout: 256-byte header + payload of
  * exactly expert_bytes[bits] bytes (quant.py:239-246 formula).  Returns

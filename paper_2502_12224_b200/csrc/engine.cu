@@ -550,6 +550,7 @@ struct fate_engine {
   int64_t host_stride[17] = {};
   std::vector<const uint8_t *> shared_dev;
   const uint8_t **shared_table_dev = nullptr;
+  int32_t *pf_shared_I = nullptr;
   cudaStream_t cstream = nullptr, xstream = nullptr;
   int max_total_I = 0;
   int prefill_max_tokens = 0;
@@ -612,6 +613,8 @@ int copy_to_buffers(fate_engine *g, const int32_t *loads_dev, int layer, int bit
 }
 
 }  // namespace
+
+static int prefill_preload();
 
 extern "C" int fate_version(void) { return 1; }
 extern "C" const char *fate_last_error(void) { return g_err.c_str(); }
@@ -736,6 +739,9 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_seed_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, run_begin_kernel));
     FATE_CUDA(ffn_preload());
+    FATE_CUDA(k4_preload());
+    FATE_CUDA(gate_preload());
+    if (int st = prefill_preload()) return st;
   }
   engine_reset_kernel<<<64, 256, 0, g->cstream>>>(d, g->caps_dev);
   FATE_CHECK_LAUNCH("engine_reset_kernel");
@@ -1209,5 +1215,675 @@ extern "C" int fate_engine_set_strategy(fate_engine *g, const fate_engine_config
   d.policy = c->policy;
   d.q = c->percentile_q;
   d.budget_n = g->cfg.budget_n;
+  return FATE_OK;
+}
+
+// ===========================================================================
+// Prefill (simulate_prefill, pipeline.py:536-778) on the device.
+//
+// Per layer l, on the compute stream:
+//   prefill_x_kernel       X = sqrt(H) * gate_in[:, l]             (fp32)
+//   K1p gate_batch x2      routing/order for layer l and for l+1 (top-k policy, pipeline.py:600)
+//   prefill_plan_kernel    chosen sets, actives + counts, popularity profile
+//                          of the l+1 predictions (prefill_merge) and its bit
+//                          map (assign_bits), prefetch list for l+1 (skip
+//                          resident), resident / requested / on-demand split of
+//                          layer l, per-expert token lists for K4, host message
+//   WAIT                   flag set once every needed copy landed
+//   K4 up/down + combine   grouped dequant-fused SwiGLU over the actives (+ shared)
+//   prefill_arc_kernel     update_after_layer(l, actives) with buffer hand-over
+// The host processes the plan message at "block end": prefetches of layer l
+// that have not been submitted yet are re-issued as on-demand loads at the
+// on-demand width (drop_stale((0, l)) + pipeline.py:701-719).
+// ===========================================================================
+
+namespace fate {
+namespace {
+
+struct PfScratch {
+  double *routing;   // [T, E] layer l
+  int32_t *order;    // [T, E] layer l
+  int32_t *order_n;  // [T, E] layer l+1
+  float *X;          // [T, H]
+  int32_t *chosen;   // [T, k] ascending
+  float *cw;         // [T, k]
+  int32_t *tok_idx;  // [T*(k+1)]
+  int32_t *zrow;     // [T*(k+1)]
+  PrefillExpert *ex; // [E+1]
+  int32_t *a_off;    // [E+1]
+  int32_t *stage;    // [E] buffer used by each active expert in this layer
+  int32_t *actives;  // [E]
+  int32_t *victims;  // [L, E+1]: count then ids
+  float *A;
+  float *Z;
+};
+
+__global__ void prefill_x_kernel(const double *gate_in, int T, int L, int layer, int H, float *X) {
+  const double sH = sqrt((double)H);
+  const int64_t n = (int64_t)T * H;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / H, h = i % H;
+    X[i] = (float)(sH * gate_in[(t * L + layer) * H + h]);
+  }
+}
+
+__device__ void sort_by_count_desc(int32_t *ids, const int32_t *cnt, int n) {
+  // insertion sort by (-count, id); n <= E <= 256, single thread
+  for (int i = 1; i < n; ++i) {
+    const int v = ids[i];
+    int j = i;
+    while (j > 0 && (cnt[ids[j - 1]] < cnt[v] || (cnt[ids[j - 1]] == cnt[v] && ids[j - 1] > v))) {
+      ids[j] = ids[j - 1];
+      --j;
+    }
+    ids[j] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) prefill_plan_kernel(EngineDev d, PfScratch s, int layer, int T, int predict,
+                                                            int reorder, double p_int2, int od_bits,
+                                                            const int32_t *__restrict__ trace_chosen,
+                                                            int32_t *shared_I_out) {
+  __shared__ int32_t cnt[EMAX], pcnt[EMAX], fill[EMAX], order[EMAX], bits_of[EMAX], mark[EMAX];
+  __shared__ int32_t first_seen[EMAX], fs_n;
+  __shared__ int mism;
+  const int E = d.E, k = d.k, L = d.L;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0, pcnt[e] = 0, fill[e] = 0, mark[e] = 0;
+  if (threadIdx.x == 0) mism = 0;
+  __syncthreads();
+  // (1) chosen sets of layer l (ascending) with their routing weights; counts
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    int32_t c[KMAX];
+    for (int j = 0; j < k; ++j) c[j] = s.order[(int64_t)t * E + j];
+    for (int i = 1; i < k; ++i)
+      for (int j = i; j > 0 && c[j - 1] > c[j]; --j) {
+        const int x = c[j];
+        c[j] = c[j - 1];
+        c[j - 1] = x;
+      }
+    for (int j = 0; j < k; ++j) {
+      s.chosen[t * k + j] = c[j];
+      s.cw[t * k + j] = (float)s.routing[(int64_t)t * E + c[j]];
+      atomicAdd(&cnt[c[j]], 1);
+      if (trace_chosen && trace_chosen[((int64_t)t * L + layer) * k + j] != c[j]) atomicExch(&mism, 1);
+    }
+    if (predict)
+      for (int j = 0; j < k; ++j) atomicAdd(&pcnt[s.order_n[(int64_t)t * E + j]], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  StepMsg *msg = d.ring + (layer % kRing);
+  if (mism) atomicAdd(&d.stats->mismatches, 1ull);
+  msg->mismatch = mism;
+  // (2) popularity profile of the predictions for l+1 (prefill_merge, assign_bits)
+  int n_pf = 0, n_pred = 0;
+  if (predict) {
+    for (int e = 0; e < E; ++e)
+      if (pcnt[e] > 0) order[n_pred++] = e;
+    sort_by_count_desc(order, pcnt, n_pred);
+    const int m = (int)floor(p_int2 * (double)n_pred);
+    for (int i = 0; i < n_pred; ++i) {
+      bits_of[order[i]] = d.prefetch_bits >= 16 ? 16 : (i >= n_pred - m ? 2 : 4);
+      msg->pred_order[i] = order[i];
+      msg->pred_cnt[i] = pcnt[order[i]];
+    }
+    int32_t *issue = order;
+    int n_issue = n_pred;
+    if (!reorder) {  // token-request order: token ascending, ids ascending within (pipeline.py:524-533)
+      fs_n = 0;
+      for (int t = 0; t < T; ++t) {
+        int32_t c[KMAX];
+        for (int j = 0; j < k; ++j) c[j] = s.order_n[(int64_t)t * E + j];
+        for (int i = 1; i < k; ++i)
+          for (int j = i; j > 0 && c[j - 1] > c[j]; --j) {
+            const int x = c[j];
+            c[j] = c[j - 1];
+            c[j - 1] = x;
+          }
+        for (int j = 0; j < k; ++j)
+          if (!mark[c[j]]) mark[c[j]] = 1, first_seen[fs_n++] = c[j];
+      }
+      for (int e = 0; e < E; ++e) mark[e] = 0;
+      issue = first_seen;
+      n_issue = fs_n;
+    }
+    for (int i = 0; i < n_issue; ++i) {
+      const int e = issue[i];
+      if (d.buf_of[(layer + 1) * E + e] >= 0 || d.pend_buf[(layer + 1) * E + e] >= 0) continue;
+      const int b = pop_free(d);
+      const uint32_t g = ++d.buf_gen[b];
+      d.buf_bits[b] = bits_of[e];
+      d.pend_buf[(layer + 1) * E + e] = b;
+      d.pend_gen[(layer + 1) * E + e] = g;
+      msg->pf_e[n_pf] = e;
+      msg->pf_b[n_pf] = b;
+      msg->pf_g[n_pf] = g;
+      msg->pf_bits_each[n_pf] = bits_of[e];
+      ++n_pf;
+    }
+    atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
+  }
+  msg->n_pred = n_pred;
+  msg->n_pf = n_pf;
+  // (3) actives of layer l and the resident / requested / on-demand split
+  int n_act = 0, n_res = 0, n_need = 0, n_od = 0, n_arr = 0, n_deq = 0;
+  bool all_landed = true;
+  for (int e = 0; e < E; ++e)
+    if (cnt[e] > 0) {
+      s.actives[n_act] = e;
+      msg->active_e[n_act] = e;
+      msg->active_cnt[n_act] = cnt[e];
+      ++n_act;
+    }
+  // recall of the layer-l prediction made one layer earlier (pipeline.py:676-680)
+  Ctrl &C = *d.ctrl;
+  if (C.pred_valid && C.pred_layer == layer && n_act > 0) {
+    int inter = 0;
+    for (int i = 0; i < C.pred_n; ++i) inter += cnt[C.pred_list[i]] > 0;
+    d.stats->recall_sum += (double)inter / (double)n_act;
+    d.stats->recall_n += 1;
+  }
+  // this layer's profile becomes the prediction checked at layer l+1
+  C.pred_valid = predict;
+  if (predict) {
+    C.pred_n = n_pred;
+    C.pred_layer = layer + 1;
+    for (int i = 0; i < n_pred; ++i) C.pred_list[i] = msg->pred_order[i];
+  }
+  int32_t *od_order = first_seen;  // reuse as scratch for the on-demand order
+  int n_unpl = 0;
+  for (int i = 0; i < n_act; ++i) {
+    const int e = s.actives[i];
+    const int b = d.buf_of[layer * E + e];
+    if (b >= 0) {
+      s.stage[e] = b;
+      msg->res_e[n_res++] = e;
+      n_deq += (d.cached_bits < 16);
+    } else if (d.pend_buf[layer * E + e] >= 0) {
+      const int pb = d.pend_buf[layer * E + e];
+      s.stage[e] = pb;
+      const bool arr = ((volatile uint32_t *)d.buf_done)[pb] == d.pend_gen[layer * E + e];
+      n_arr += arr;
+      all_landed = all_landed && arr;
+      msg->need_e[n_need] = e;
+      msg->need_b[n_need] = pb;
+      ++n_need;
+    } else {
+      od_order[n_unpl++] = e;
+    }
+  }
+  if (reorder) sort_by_count_desc(od_order, cnt, n_unpl);
+  else {  // first-seen order of this layer's chosen sets
+    int nfs = 0;
+    for (int t = 0; t < T && nfs < n_unpl; ++t)
+      for (int j = 0; j < k; ++j) {
+        const int e = s.chosen[t * k + j];
+        bool unpl = false;
+        for (int i = 0; i < n_unpl; ++i) unpl |= od_order[i] == e;
+        if (unpl && !mark[e]) mark[e] = 1, fill[nfs++] = e;
+      }
+    for (int i = 0; i < n_unpl; ++i) od_order[i] = fill[i];
+    for (int e = 0; e < E; ++e) mark[e] = 0, fill[e] = 0;
+  }
+  for (int i = 0; i < n_unpl; ++i) {
+    const int e = od_order[i];
+    const int b = pop_free(d);
+    const uint32_t g = ++d.buf_gen[b];
+    d.buf_bits[b] = od_bits;
+    s.stage[e] = b;
+    msg->od_e[n_od] = e;
+    msg->od_b[n_od] = b;
+    msg->od_g[n_od] = g;
+    ++n_od;
+    all_landed = false;
+  }
+  // prefetched for l but inactive: release + drop (pipeline.py:682)
+  int n_drop = 0;
+  for (int e = 0; e < E; ++e) {
+    const int b = d.pend_buf[layer * E + e];
+    if (b < 0) continue;
+    d.pend_buf[layer * E + e] = -1;
+    if (cnt[e] > 0) continue;
+    msg->drop_e[n_drop] = e;
+    msg->drop_b[n_drop] = b;
+    ++n_drop;
+    push_free(d, b);
+  }
+  // (4) token lists per active expert, in ascending expert order, tokens ascending
+  int off = 0;
+  int64_t aoff = 0;
+  for (int i = 0; i < n_act; ++i) {
+    const int e = s.actives[i];
+    fill[e] = off;
+    s.ex[i] = PrefillExpert{d.pool + (int64_t)s.stage[e] * d.buf_stride, d.I, 0, off, cnt[e]};
+    s.a_off[i] = (int32_t)aoff;
+    off += cnt[e];
+    aoff += (int64_t)cnt[e] * d.I;
+  }
+  for (int t = 0; t < T; ++t)
+    for (int j = 0; j < k; ++j) {
+      const int e = s.chosen[t * k + j];
+      const int pos = fill[e]++;
+      s.tok_idx[pos] = t;
+      s.zrow[pos] = t * (k + 1) + j;
+    }
+  int n_ex = n_act;
+  if (d.shared && d.shared[layer]) {
+    const int Is = d.I_shared;
+    s.ex[n_ex] = PrefillExpert{d.shared[layer], Is, 0, off, T};
+    s.a_off[n_ex] = (int32_t)aoff;
+    for (int t = 0; t < T; ++t) {
+      s.tok_idx[off + t] = t;
+      s.zrow[off + t] = t * (k + 1) + k;
+    }
+    ++n_ex;
+    *shared_I_out = Is;
+  } else {
+    *shared_I_out = 0;
+  }
+  // src bits: resident -> cached, requested -> its prefetch width, on-demand -> od width
+  for (int i = 0; i < n_need; ++i) n_deq += (d.buf_bits[msg->need_b[i]] < 16);
+  n_deq += n_od * (od_bits < 16);
+  msg->n_active = n_act;
+  msg->n_res = n_res;
+  msg->n_need = n_need;
+  msg->n_od = n_od;
+  msg->n_drop = n_drop;
+  msg->od_bits = od_bits;
+  msg->pf_bits = d.prefetch_bits;
+  msg->step = layer;
+  msg->token = 0;
+  msg->layer = layer;
+  atomicAdd(&d.stats->accesses, (unsigned long long)n_act);
+  atomicAdd(&d.stats->cache_hits, (unsigned long long)n_res);
+  atomicAdd(&d.stats->arrival_hits, (unsigned long long)n_arr);
+  atomicAdd(&d.stats->ondemand_issued, (unsigned long long)n_od);
+  atomicAdd(&d.stats->dequant_count, (unsigned long long)n_deq);
+  const int self = all_landed ? 1 : 0;
+  msg->self_signaled = self;
+  if (self) ((volatile uint32_t *)d.ready)[layer] = 1u;
+  __threadfence_system();
+  msg->seq = (uint32_t)layer + 1u;
+  __threadfence_system();
+}
+
+// update_after_layer(l, actives) with buffer hand-over (cf. apply_prev_update).
+__global__ void prefill_arc_kernel(EngineDev d, PfScratch s, int layer, int n_act) {
+  __shared__ ArcLayer arc_sm;
+  __shared__ int32_t rel[EMAX + 4];
+  const int lane = threadIdx.x;
+  WarpArc arc;
+  arc.load(&d.arc[layer], &arc_sm);
+  int nrel = 0, nvic = 0;
+  int32_t *vic = s.victims + (int64_t)layer * (d.E + 1);
+  for (int i = 0; i < n_act; ++i) {
+    const int e = s.actives[i];
+    int victim;
+    const int hit = arc.access(e, &victim);
+    if (lane == 0) {
+      if (victim >= 0) {
+        int32_t &slot = d.buf_of[layer * d.E + victim];
+        if (slot >= 0) rel[nrel++] = slot;
+        slot = -1;
+        vic[1 + nvic++] = victim;
+      }
+      if (!hit) {
+        const int b = s.stage[e];
+        if (arc.c >= 1) {
+          d.buf_of[layer * d.E + e] = b;
+          for (int r = 0; r < nrel; ++r)
+            if (rel[r] == b) rel[r] = rel[--nrel], r = nrel;
+        } else {
+          rel[nrel++] = b;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  arc.store(&d.arc[layer]);
+  if (lane == 0) {
+    for (int r = 0; r < nrel; ++r) push_free(d, rel[r]);
+    vic[0] = nvic;
+  }
+}
+
+__global__ void prefill_begin_kernel(EngineDev d) {
+  Ctrl &C = *d.ctrl;
+  C.pred_valid = 0;
+  C.err = 0;
+  for (int i = 0; i < d.L * d.E; ++i) {
+    if (d.pend_buf[i] >= 0) push_free(d, d.pend_buf[i]);
+    d.pend_buf[i] = -1;
+  }
+  *d.stats = DevStats{};
+}
+
+}  // namespace
+}  // namespace fate
+
+static int ensure_prefill_scratch(fate_engine *g, PfScratch &s, int T) {
+  const int E = g->cfg.num_experts, k = g->cfg.top_k, H = g->cfg.hidden_dim, L = g->cfg.num_layers;
+  const int Tm = g->cfg.max_tokens;
+  const int64_t a_floats = (int64_t)Tm * k * g->cfg.intermediate_dim + (int64_t)Tm * g->cfg.shared_intermediate;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = off;
+    off = (size_t)align_up((int64_t)(off + bytes), 256);
+    return o;
+  };
+  const size_t o_r = carve((size_t)Tm * E * 8), o_o = carve((size_t)Tm * E * 4), o_on = carve((size_t)Tm * E * 4),
+               o_x = carve((size_t)Tm * H * 4), o_c = carve((size_t)Tm * k * 4), o_cw = carve((size_t)Tm * k * 4),
+               o_ti = carve((size_t)Tm * (k + 1) * 4), o_zr = carve((size_t)Tm * (k + 1) * 4),
+               o_ex = carve(sizeof(PrefillExpert) * (E + 1)), o_ao = carve(4 * (E + 1)), o_st = carve(4 * E),
+               o_ac = carve(4 * E), o_v = carve(4 * (size_t)L * (E + 1)), o_si = carve(16),
+               o_A = carve(4 * (size_t)a_floats), o_Z = carve(4 * (size_t)Tm * (k + 1) * H);
+  if (!g->pf_block) FATE_CUDA(cudaMalloc(&g->pf_block, off));
+  uint8_t *b = (uint8_t *)g->pf_block;
+  s.routing = (double *)(b + o_r);
+  s.order = (int32_t *)(b + o_o);
+  s.order_n = (int32_t *)(b + o_on);
+  s.X = (float *)(b + o_x);
+  s.chosen = (int32_t *)(b + o_c);
+  s.cw = (float *)(b + o_cw);
+  s.tok_idx = (int32_t *)(b + o_ti);
+  s.zrow = (int32_t *)(b + o_zr);
+  s.ex = (PrefillExpert *)(b + o_ex);
+  s.a_off = (int32_t *)(b + o_ao);
+  s.stage = (int32_t *)(b + o_st);
+  s.actives = (int32_t *)(b + o_ac);
+  s.victims = (int32_t *)(b + o_v);
+  g->pf_shared_I = (int32_t *)(b + o_si);
+  s.A = (float *)(b + o_A);
+  s.Z = (float *)(b + o_Z);
+  (void)T;
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, const int32_t *chosen_dev, int T,
+                                   float *Y_dev, fate_prefill_log *log_host, fate_run_stats *stats) {
+  std::lock_guard<std::mutex> lock(g->mu);
+  const int L = g->cfg.num_layers, E = g->cfg.num_experts, k = g->cfg.top_k, H = g->cfg.hidden_dim;
+  const int I = g->cfg.intermediate_dim;
+  if (T < 1 || T > g->cfg.max_tokens) {
+    set_error("fate_engine_prefill: T must lie in [1, max_tokens]");
+    return FATE_EINVAL;
+  }
+  const int predict = g->cfg.prefill_use_predictor && g->cfg.use_predictor;
+  const int od_bits = g->cfg.prefill_ondemand_bits;
+  if (!g->host_pool[od_bits] || (predict && g->cfg.prefetch_bits < 16 && (!g->host_pool[4] || !g->host_pool[2])) ||
+      (predict && g->cfg.prefetch_bits >= 16 && !g->host_pool[16])) {
+    set_error("fate_engine_prefill: pinned host pool missing for the strategy's bit widths");
+    return FATE_EINVAL;
+  }
+  cudaSetDevice(g->cfg.device);
+  PfScratch s;
+  if (int st = ensure_prefill_scratch(g, s, T)) return st;
+  const cudaStream_t cs = g->cstream;
+  const bool timed = stats != nullptr;
+  const bool dbg = getenv("FATE_DEBUG") != nullptr;
+  Channel ch;
+  ch.g = g;
+  ch.timed = timed;
+  std::vector<cudaEvent_t> kev;
+  if (timed) {
+    ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
+    for (auto &e : ch.ev) FATE_CUDA(cudaEventCreate(&e));
+    for (int i = (int)ch.ev.size() - 2; i >= 0; i -= 2) ch.ev_free.push_back(i);
+    kev.resize(4 * (size_t)L);
+    for (auto &e : kev) FATE_CUDA(cudaEventCreate(&e));
+    ch.t0 = kev[0];
+  }
+  g->step_ms.clear();
+  g->copy_ms.clear();
+  g->copy_meta.clear();
+  for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
+  *g->copy_done_host = 0;
+  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
+  EngineDev d = g->d;
+  d.ready = g->ready_dev;
+  prefill_begin_kernel<<<1, 1, 0, cs>>>(d);
+  FATE_CHECK_LAUNCH("prefill_begin_kernel");
+  FATE_CUDA(cudaStreamSynchronize(cs));
+  double flops = 0.0;
+  int status = FATE_OK;
+  std::vector<double> tau(L);
+  FATE_CUDA(cudaMemcpy(tau.data(), g->d.tau, L * 8, cudaMemcpyDeviceToHost));
+  auto launch_front = [&](int l) -> int {
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l], cs));
+    prefill_x_kernel<<<148 * 4, 256, 0, cs>>>(gate_in_dev, T, L, l, H, s.X);
+    FATE_CHECK_LAUNCH("prefill_x_kernel");
+    FATE_CUDA(launch_gate_batch(g->d.W + (int64_t)l * E * H, tau[l], gate_in_dev + (int64_t)l * H, (int64_t)L * H, T,
+                                E, H, s.routing, s.order, nullptr, k, 0, 0.5, cs));
+    const int pred_here = predict && l + 1 < L;
+    if (pred_here)
+      FATE_CUDA(launch_gate_batch(g->d.W + (int64_t)(l + 1) * E * H, tau[l + 1], gate_in_dev + (int64_t)l * H,
+                                  (int64_t)L * H, T, E, H, nullptr, s.order_n, nullptr, k, 0, 0.5, cs));
+    prefill_plan_kernel<<<1, 1024, 0, cs>>>(d, s, l, T, pred_here, g->cfg.reorder_prefill, g->cfg.p_int2, od_bits,
+                                            chosen_dev, g->pf_shared_I);
+    FATE_CHECK_LAUNCH("prefill_plan_kernel");
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l + 1], cs));
+    return FATE_OK;
+  };
+  if ((status = launch_front(0))) return status;
+  std::vector<int> pf_bits_cur(E, 0);  // widths of the prefetches issued for the current layer
+  auto last_progress = std::chrono::steady_clock::now();
+  for (int l = 0; l < L && status == FATE_OK; ++l) {
+    StepMsg &m = g->ring_host[l % kRing];
+    while (m.seq != (uint32_t)l + 1u) {
+      if ((status = ch.pump())) break;
+      _mm_pause();
+      if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(60)) {
+        status = FATE_ETIMEOUT;
+        set_error("fate_engine_prefill: no plan message for 60 s");
+        break;
+      }
+    }
+    if (status) break;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    last_progress = std::chrono::steady_clock::now();
+    fate_prefill_log *lg = log_host ? log_host + l : nullptr;
+    if (lg) memset(lg, 0, sizeof(*lg));
+    // drop prefetches of layer l the gate did not activate
+    for (int i = 0; i < m.n_drop; ++i) {
+      auto it = std::find_if(ch.pending.begin(), ch.pending.end(),
+                             [&](const Transfer &x) { return x.kind == 0 && x.layer == l && x.expert == m.drop_e[i]; });
+      if (it != ch.pending.end()) ch.pending.erase(it), ++ch.dropped;
+    }
+    // block end: requested prefetches that have not started become on-demand loads
+    std::vector<int> started, converted;
+    for (int i = 0; i < m.n_need; ++i) {
+      const int e = m.need_e[i];
+      auto it = std::find_if(ch.pending.begin(), ch.pending.end(),
+                             [&](const Transfer &x) { return x.kind == 0 && x.layer == l && x.expert == e; });
+      if (it != ch.pending.end()) {
+        Transfer t = *it;
+        ch.pending.erase(it);
+        ++ch.dropped;
+        converted.push_back(e);
+        (void)t;
+      } else {
+        started.push_back(e);
+      }
+    }
+    std::vector<int> cnt(E, 0);
+    for (int i = 0; i < m.n_active; ++i) cnt[m.active_e[i]] = m.active_cnt[i];
+    // the on-demand set in (-count, id) order (pipeline.py:703-704); non-reordered strategies keep device order
+    std::vector<std::pair<int, int>> od;  // expert, buffer
+    std::vector<uint32_t> od_gen;
+    for (int i = 0; i < m.n_od; ++i) od.push_back({m.od_e[i], m.od_b[i]});
+    for (int i = 0; i < m.n_od; ++i) od_gen.push_back(m.od_g[i]);
+    for (int e : converted) {
+      int b = -1;
+      for (int i = 0; i < m.n_need; ++i)
+        if (m.need_e[i] == e) b = m.need_b[i];
+      od.push_back({e, b});
+      od_gen.push_back(0);
+    }
+    std::vector<int> idx(od.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+    if (g->cfg.reorder_prefill)
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+        const int ea = od[a].first, eb = od[b].first;
+        return cnt[ea] != cnt[eb] ? cnt[ea] > cnt[eb] : ea < eb;
+      });
+    // prefetches for l+1 (issued at predict_at, before this layer's on-demand loads)
+    for (int i = 0; i < m.n_pf; ++i)
+      ch.pending.push_back(Transfer{0, 0, l + 1, m.pf_e[i], m.pf_bits_each[i], m.pf_b[i], m.pf_g[i], -1, -1});
+    for (int i : idx) {
+      // converted prefetches reuse their buffer; bump the generation by the device's next value
+      uint32_t gen = od_gen[i];
+      ch.pending.push_back(Transfer{1, 0, l, od[i].first, od_bits, od[i].second, gen, -1, -1});
+    }
+    ch.promote();
+    if (!m.self_signaled) {
+      int last = -1;
+      for (int i = 0; i < (int)ch.pending.size(); ++i)
+        if (ch.pending[i].kind == 1 && ch.pending[i].layer == l) last = i;
+      if (last >= 0) {
+        ch.pending[last].signal_token = 0;
+        ch.pending[last].signal_layer = l;
+      } else {
+        ch.pending.push_front(Transfer{2, 0, l, -1, 0, -1, 0, 0, l});
+      }
+    }
+    if ((status = ch.pump())) break;
+    // host log (timing-independent fields + this run's started set)
+    if (lg) {
+      lg->n_pred = m.n_pred;
+      for (int i = 0; i < m.n_pred; ++i) lg->pred_order[i] = m.pred_order[i], lg->pred_counts[i] = m.pred_cnt[i];
+      lg->n_prefetch = m.n_pf;
+      for (int i = 0; i < m.n_pf; ++i) lg->prefetch[i] = m.pf_e[i], lg->prefetch_bits[i] = m.pf_bits_each[i];
+      lg->n_active = m.n_active;
+      for (int i = 0; i < m.n_active; ++i) lg->actives[i] = m.active_e[i], lg->counts[i] = m.active_cnt[i];
+      lg->n_resident = m.n_res;
+      for (int i = 0; i < m.n_res; ++i) lg->resident[i] = m.res_e[i];
+      lg->n_started = (int)started.size();
+      lg->n_planned = (int)started.size();
+      for (size_t i = 0; i < started.size(); ++i) lg->started[i] = started[i], lg->planned[i] = started[i];
+      lg->n_ondemand = (int)idx.size();
+      for (size_t i = 0; i < idx.size(); ++i) lg->ondemand[i] = od[idx[i]].first;
+      lg->mismatch = m.mismatch;
+      for (int i = 0; i < m.n_active; ++i) {
+        const int e = m.active_e[i];
+        int b = g->cfg.cached_bits < 16 ? g->cfg.cached_bits : 16;  // resident (pipeline.py:689)
+        if (std::find(started.begin(), started.end(), e) != started.end()) b = pf_bits_cur[e];
+        for (size_t j = 0; j < od.size(); ++j)
+          if (od[j].first == e) b = od_bits;
+        lg->src_bits[i] = b;
+      }
+    }
+    for (int e = 0; e < E; ++e) pf_bits_cur[e] = 0;
+    for (int i = 0; i < m.n_pf; ++i) pf_bits_cur[m.pf_e[i]] = m.pf_bits_each[i];
+    // expert compute for layer l once every needed copy landed
+    FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), 1u, CU_STREAM_WAIT_VALUE_GEQ));
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l + 2], cs));
+    int tiles_up = 0, tiles_down = 0;
+    for (int i = 0; i < m.n_active; ++i) {
+      tiles_up += k4_tiles(m.active_cnt[i], I, H, false);
+      tiles_down += k4_tiles(m.active_cnt[i], I, H, true);
+      flops += 6.0 * H * I * m.active_cnt[i];
+    }
+    int n_ex = m.n_active;
+    const int has_shared = g->cfg.shared_intermediate && g->shared_dev[l] ? 1 : 0;
+    if (has_shared) {
+      tiles_up += k4_tiles(T, g->cfg.shared_intermediate, H, false);
+      tiles_down += k4_tiles(T, g->cfg.shared_intermediate, H, true);
+      flops += 6.0 * H * g->cfg.shared_intermediate * T;
+      ++n_ex;
+    }
+    FATE_CUDA(launch_k4_simt(s.X, H, s.ex, n_ex, s.tok_idx, s.zrow, s.a_off, s.A, s.Z, tiles_up, tiles_down, cs));
+    FATE_CUDA(launch_k4_combine(s.Z, s.cw, T, k, H, has_shared, Y_dev + (int64_t)l * T * H, cs));
+    prefill_arc_kernel<<<1, 32, 0, cs>>>(d, s, l, m.n_active);
+    FATE_CHECK_LAUNCH("prefill_arc_kernel");
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l + 3], cs));
+    if (l + 1 < L && (status = launch_front(l + 1))) break;
+    if (dbg) fprintf(stderr, "[fate] prefill layer %d act=%d res=%d need=%d started=%zu od=%zu pf=%d\n", l, m.n_active,
+                     m.n_res, m.n_need, started.size(), idx.size(), m.n_pf);
+  }
+  if (status != FATE_OK)
+    for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
+  auto drain_start = std::chrono::steady_clock::now();
+  while (status == FATE_OK && (!ch.pending.empty() || !ch.inflight.empty())) {
+    ch.pending.erase(std::remove_if(ch.pending.begin(), ch.pending.end(),
+                                    [&](const Transfer &x) { return x.kind == 0 && x.layer >= L; }),
+                     ch.pending.end());
+    if ((status = ch.pump())) break;
+    _mm_pause();
+    if (std::chrono::steady_clock::now() - drain_start > std::chrono::seconds(60)) {
+      status = FATE_ETIMEOUT;
+      set_error("fate_engine_prefill: copies never completed while draining");
+      for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
+    }
+  }
+  cudaError_t se = cudaStreamSynchronize(cs), xe = cudaStreamSynchronize(g->xstream);
+  if (status == FATE_OK && se != cudaSuccess) status = cuda_status(se, "prefill compute stream");
+  if (status == FATE_OK && xe != cudaSuccess) status = cuda_status(xe, "prefill copy stream");
+  DevStats ds{};
+  fate_run_stats st{};
+  if (status == FATE_OK) {
+    FATE_CUDA(cudaMemcpy(&ds, g->d.stats, sizeof(ds), cudaMemcpyDeviceToHost));
+    Ctrl cc;
+    FATE_CUDA(cudaMemcpy(&cc, g->d.ctrl, sizeof(cc), cudaMemcpyDeviceToHost));
+    if (cc.err) {
+      set_error("fate_engine_prefill: staging buffer pool exhausted");
+      status = FATE_ENOMEM;
+    }
+    if (log_host) {
+      std::vector<int32_t> vic((size_t)L * (E + 1));
+      FATE_CUDA(cudaMemcpy(vic.data(), s.victims, vic.size() * 4, cudaMemcpyDeviceToHost));
+      for (int l = 0; l < L; ++l) {
+        fate_prefill_log &lg = log_host[l];
+        lg.n_victims = vic[(size_t)l * (E + 1)];
+        for (int i = 0; i < lg.n_victims; ++i) lg.victims[i] = vic[(size_t)l * (E + 1) + 1 + i];
+      }
+    }
+  }
+  if (timed && status == FATE_OK) {
+    g->step_ms.assign(4 * (size_t)L, 0.0);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, kev[0], kev[4 * (L - 1) + 3]);
+    st.gpu_ms = ms;
+    double ffn = 0.0, gate = 0.0;
+    for (int l = 0; l < L; ++l) {
+      float t[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < 4; ++j)
+        if (l || j) cudaEventElapsedTime(&t[j], kev[0], kev[4 * l + j]);
+      for (int j = 0; j < 4; ++j) g->step_ms[4 * (size_t)l + j] = t[j];
+      gate += t[1] - t[0];
+      ffn += t[3] - t[2];
+    }
+    st.ffn_ms = ffn;
+    st.gate_ms = gate;
+  }
+  if (timed) {
+    for (auto &e : ch.ev) cudaEventDestroy(e);
+    for (auto &e : kev) cudaEventDestroy(e);
+  }
+  st.steps = L;
+  st.accesses = (int64_t)ds.accesses;
+  st.cache_hits = (int64_t)ds.cache_hits;
+  st.arrival_hits = (int64_t)ds.arrival_hits;
+  st.dequant_count = (int64_t)ds.dequant_count;
+  st.prefetch_issued = (int64_t)ds.prefetch_issued;
+  st.ondemand_issued = (int64_t)ds.ondemand_issued;
+  st.transfers_done = ch.done;
+  st.transfers_dropped = ch.dropped;
+  st.h2d_bytes = ch.h2d_bytes;
+  st.copy_busy_ms = ch.copy_ms;
+  st.recall_sum = ds.recall_sum;
+  st.recall_n = (int64_t)ds.recall_n;
+  st.trace_mismatches = (int64_t)ds.mismatches;
+  st.ffn_flops = flops;
+  st.error = status;
+  if (stats) *stats = st;
+  return status;
+}
+
+static int prefill_preload() {
+  cudaFuncAttributes fa;
+  FATE_CUDA(cudaFuncGetAttributes(&fa, prefill_x_kernel));
+  FATE_CUDA(cudaFuncGetAttributes(&fa, prefill_plan_kernel));
+  FATE_CUDA(cudaFuncGetAttributes(&fa, prefill_arc_kernel));
+  FATE_CUDA(cudaFuncGetAttributes(&fa, prefill_begin_kernel));
   return FATE_OK;
 }

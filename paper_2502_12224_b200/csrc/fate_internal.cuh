@@ -119,7 +119,7 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *x_d
 cudaError_t ffn_preload();
 
 // K1 kernels exposed to the engine.
-cudaError_t launch_gate_batch(const double *W, double tau, const double *h, int T, int E, int H,
+cudaError_t launch_gate_batch(const double *W, double tau, const double *h, int64_t h_stride, int T, int E, int H,
                               double *routing, int32_t *order, int32_t *list_len, int top_k, int policy,
                               double q, cudaStream_t s);
 
@@ -132,8 +132,13 @@ struct PrefillExpert {
   int n_tok;
 };
 
-cudaError_t launch_ffn_prefill(const float *X, int T, int H, int n, const PrefillExpert *experts_dev,
-                               const int32_t *tok_idx, const float *tok_w, float *Y, int max_I,
-                               int max_tok, float *scratch, cudaStream_t s);
+cudaError_t launch_k4_simt(const float *X, int H, const PrefillExpert *ex_dev, int n, const int32_t *tok_idx,
+                           const int32_t *zrow, const int *a_off_dev, float *A, float *Z, int tiles_up,
+                           int tiles_down, cudaStream_t s);
+cudaError_t launch_k4_combine(const float *Z, const float *w, int T, int k, int H, int has_shared, float *Y,
+                              cudaStream_t s);
+cudaError_t k4_preload();
+cudaError_t gate_preload();
+int k4_tiles(int n_tok, int I, int H, bool down);
 
 }  // namespace fate

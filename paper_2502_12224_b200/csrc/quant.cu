@@ -84,6 +84,18 @@ __global__ void dequant_kernel(const uint8_t *__restrict__ codes, const float2 *
   }
 }
 
+// fp64 dequantization with the reference's rounding: zero + (code * scale),
+// two roundings, no contraction (quant.py:119).
+__global__ void dequant64_kernel(const uint8_t *__restrict__ codes, const double *__restrict__ s64,
+                                 const double *__restrict__ z64, int64_t n, int bits, int group,
+                                 double *__restrict__ out) {
+  const int per_byte = 8 / bits;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (codes[i / per_byte] >> ((i % per_byte) * bits)) & ((1u << bits) - 1);
+    out[i] = __dadd_rn(z64[i / group], __dmul_rn((double)c, s64[i / group]));
+  }
+}
+
 __global__ void write_header_kernel(uint8_t *dst, int bits, int layer, int expert, int H, int I) {
   ExpertHeader *h = reinterpret_cast<ExpertHeader *>(dst);
   const int t = threadIdx.x;
@@ -162,6 +174,19 @@ extern "C" int fate_dequant(const uint8_t *codes_dev, const float *sz_dev, int64
   dequant_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       codes_dev, reinterpret_cast<const float2 *>(sz_dev), n, bits, group, out_dev);
   FATE_CHECK_LAUNCH("dequant_kernel");
+  return FATE_OK;
+}
+
+extern "C" int fate_dequant64(const uint8_t *codes_dev, const double *scale64_dev, const double *zero64_dev,
+                              int64_t n, int bits, int group, double *out_dev, void *stream) {
+  if (n < 0 || group < 1 || !(bits == 2 || bits == 4 || bits == 8)) {
+    set_error("fate_dequant64: bad arguments");
+    return FATE_EINVAL;
+  }
+  if (n == 0) return FATE_OK;
+  dequant64_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(codes_dev, scale64_dev, zero64_dev, n, bits,
+                                                                        group, out_dev);
+  FATE_CHECK_LAUNCH("dequant64_kernel");
   return FATE_OK;
 }
 

@@ -70,6 +70,14 @@ def dequant(codes: torch.Tensor, sz: torch.Tensor, n: int, bits: int, group: int
     return out
 
 
+def dequant64(codes: torch.Tensor, s64: torch.Tensor, z64: torch.Tensor, n: int, bits: int,
+              group: int = 64) -> torch.Tensor:
+    L = _lib.lib()
+    out = torch.empty((n,), dtype=torch.float64, device=codes.device)
+    check(L.fate_dequant64(ptr(codes), ptr(s64), ptr(z64), n, bits, group, ptr(out), _stream()), "fate_dequant64")
+    return out
+
+
 def expert_buffer_bytes(H: int, I: int, bits: int) -> int:
     v = _lib.load().fate_expert_buffer_bytes(H, I, bits)
     if v < 0:
