@@ -521,3 +521,40 @@ def unpack_buffer(buf: np.ndarray, H: int, I: int, bits: int) -> dict:
         out["w" + j] = dequantize(codes, sz[:, 0].astype(np.float64), sz[:, 1].astype(np.float64), bits,
                                   shapes[j])
     return out
+
+
+# ---------------------------------------------------------------------------
+# C restatement of the expert FFN (oracle/ffn_cpu.c), for CPU timing only
+
+
+def cpu_lib():
+    import ctypes
+    import os
+    import subprocess
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    so = os.path.join(here, "libfate_oracle.so")
+    if not os.path.exists(so):
+        subprocess.run(["make", "-s", "-C", here], check=True)
+    lib = ctypes.CDLL(so)
+    P = ctypes.POINTER
+    lib.fate_cpu_ffn.argtypes = [P(ctypes.c_float), ctypes.c_int, ctypes.c_int, P(ctypes.c_void_p), P(ctypes.c_int),
+                                 P(ctypes.c_int), P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float)]
+    lib.fate_cpu_ffn.restype = None
+    lib.fate_cpu_threads.argtypes = [ctypes.c_int]
+    lib.fate_cpu_threads.restype = ctypes.c_int
+    return lib
+
+
+def cpu_ffn(lib, x: np.ndarray, bufs: list, I: list, bits: list, w: list, scratch: np.ndarray) -> np.ndarray:
+    import ctypes
+
+    n = len(bufs)
+    H = x.shape[0]
+    y = np.empty(H, np.float32)
+    arr = (ctypes.c_void_p * n)(*[b.ctypes.data for b in bufs])
+    f = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))  # noqa: E731
+    xc = np.ascontiguousarray(x, np.float32)
+    lib.fate_cpu_ffn(f(xc), H, n, arr, (ctypes.c_int * n)(*I), (ctypes.c_int * n)(*bits), (ctypes.c_float * n)(*w),
+                     f(y), f(scratch))
+    return y

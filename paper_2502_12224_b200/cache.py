@@ -12,7 +12,8 @@ runs with it; seeds issued before that are applied at binding time.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+import weakref
+from dataclasses import dataclass
 from typing import Iterable, Sequence
 
 from .core import ModelConfig
@@ -74,7 +75,9 @@ class _LayerView:
     """``cache.layers[l]``: the ArcState-like view of one layer on the device."""
 
     def __init__(self, cache: "LayeredExpertCache", layer: int):
-        self._c, self.layer = cache, layer
+        # a proxy, not a reference: the cache must die by refcount so its
+        # pooled engine returns to the pool promptly (pipeline.bind_engine)
+        self._c, self.layer = weakref.proxy(cache), layer
 
     @property
     def capacity(self) -> int:

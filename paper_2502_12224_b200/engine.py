@@ -53,7 +53,7 @@ class OffloadEngine:
     def __init__(self, cfg: ModelConfig, capacities, store: ExpertStore, weights, knobs: StrategyKnobs,
                  max_tokens: int = 1024, device: int | None = None):
         self._L = _lib.lib()
-        self.cfg, self.store = cfg, store
+        self.cfg, self.store, self.weights = cfg, store, weights
         self.caps = np.ascontiguousarray(np.asarray(capacities, dtype=np.int32))
         if self.caps.shape != (cfg.num_layers,):
             raise InvalidConfig("one capacity per layer required")

@@ -164,15 +164,39 @@ def _bits_needed(strategy: Strategy, plan: CachePlan) -> tuple:
     return tuple(sorted(b))
 
 
+_IDLE: dict = {}
+
+
+def _release(key, eng) -> None:
+    _IDLE.setdefault(key, []).append(eng)
+
+
 def bind_engine(cache: LayeredExpertCache | None, plan: CachePlan, cfg: ModelConfig, weights, experts, knobs,
                 max_tokens: int):
-    """The engine of ``cache`` (created on first use), switched to ``knobs``."""
+    """The engine of ``cache`` (created on first use), switched to ``knobs``.
+
+    Engines are pooled per (expert store, plan, gate weights): a fresh
+    LayeredExpertCache takes an idle engine, resets its device cache state
+    (the reference's ``LayeredExpertCache(plan)``) and returns it to the pool
+    when the cache object is garbage collected."""
+    import weakref
+
     from .engine import OffloadEngine
 
     cache = cache if cache is not None else LayeredExpertCache(plan)
     if cache.engine is None:
-        eng = OffloadEngine(cfg, plan.per_layer_capacity, experts, weights, knobs, max_tokens=max_tokens)
+        key = (id(experts), tuple(plan.per_layer_capacity), id(weights))
+        idle = [e for e in _IDLE.get(key, []) if e.max_tokens >= max_tokens]
+        if idle:
+            eng = idle[0]
+            _IDLE[key].remove(eng)
+            eng.set_strategy(knobs)
+            eng.reset_cache()
+        else:
+            eng = OffloadEngine(cfg, plan.per_layer_capacity, experts, weights, knobs,
+                                max_tokens=max(max_tokens, 64))
         cache.bind(eng)
+        weakref.finalize(cache, _release, key, eng)
     else:
         eng = cache.engine
         if eng.max_tokens < max_tokens:
@@ -346,8 +370,6 @@ def compare_strategies(cfg: ModelConfig, timing: TimingModel, strategies: Sequen
                 rows.append(ComparisonRow(s.kind, "prefill", budget, rep, tl))
             tl, rep = simulate_decoding(decode_trace, s, plan, timing, cfg, weights=weights, cache=cache, **kw)
             rows.append(ComparisonRow(s.kind, "decoding", budget, rep, tl))
-            if cache.engine is not None:
-                cache.engine.close()
     return rows
 
 
