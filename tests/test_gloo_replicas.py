@@ -1,0 +1,63 @@
+"""World-size-2 gloo test of the replica plumbing (CPU, no GPU needed).
+
+Each rank plays one GPU: its own request stream (seed = rank), its own cache
+plan, the timing-independent decode schedule computed by the oracle, then the
+end-of-run aggregation (sum tokens, max time, summed counters)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import fate_oracle as O
+    from paper_2502_12224_b200 import core, gatesim, replicas
+    r, ws, lr = replicas.world()
+    cfg = core.ModelConfig.from_shape(4, 8, 2, 256, 512, 1)
+    tr, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=replicas.replica_seed(r), num_tokens=8))
+    _, g, ch = tr.dense_arrays(cfg)
+    caps = O.plan_capacities(4, 8, 1, 12)
+    sched = O.decode_schedule(g, ch.tolist(), np.stack(w.matrices), np.array(w.temperatures), caps, 2, 0,
+                              O.StrategyKnobs(), 4)
+    agg = replicas.aggregate(tokens=8, seconds=1.0 + r, counters={"hits": sched["cache_hits"]})
+    mine = [(l, e) for (l, e) in replicas.shard_experts(4, 8, r, ws)]
+    q.put((r, agg, sched["cache_hits"], len(mine), int(ch[0, 0, 0])))
+    dist.destroy_process_group()
+
+
+def test_two_rank_replicas_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, a0, h0, n0, c0), (r1, a1, h1, n1, c1) = out
+    assert a0 == a1                                   # every rank sees the same aggregate
+    assert a0["tokens"] == 16 and a0["seconds"] == 2.0  # sum of tokens, max of times
+    assert a0["tokens_per_s"] == 8.0
+    assert a0["hits"] == h0 + h1
+    assert n0 + n1 == 32 and n0 == 16                 # expert homes partition (l*E+e) mod G
+    from paper_2502_12224_b200 import replicas
+    assert replicas.home_rank(1, 3, 8, 2) == 1
