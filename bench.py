@@ -278,7 +278,7 @@ def main():
 
     # -- e2e through the public API: host GateTrace in, last-layer outputs back to host
     e2e_times, h2d_b, d2h_b = [], 0, 0
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_steps + 1 if args.e2e_steps else 0):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tl, rep, res = P.simulate_decoding(trace, strategy, plan, timing, cfg, weights=weights,
@@ -290,7 +290,7 @@ def main():
         h2d_b = g.nbytes + ch.nbytes
         d2h_b = y_last.numel() * 4
         res.y = None
-    e2e = T / float(np.mean(e2e_times)) * world
+    e2e = T / float(np.mean(e2e_times)) * world if e2e_times else None
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -326,7 +326,8 @@ def main():
                          "bytes_per_launch": k3_bytes, "ms_per_launch": k3_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b},
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b}
+            if e2e else None,
             "gpu_launches": int(args.steps * (3 * agg["steps"] + 2)),
             "clocks": clocks,
             "hit_rate_cache": agg["cache_hits"] / agg["accesses"],

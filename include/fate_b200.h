@@ -99,6 +99,13 @@ int fate_gate_forward(const double *W_dev, double tau, const double *h_dev, int 
 int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *const *bufs, const float *weights,
                     float *scratch_dev, float *y_dev, void *stream);
 
+/* Diagnostics: per-CTA phase timestamps (globaltimer ns) of the last K3
+ * launch, out_host[160*8]: start, consumers start, x layouts done, phase A
+ * done, grid barrier passed, activation layouts done, phase B done, producer done. */
+int fate_k3_profile(uint64_t *out_host);
+/* Diagnostics: phase timestamps of the last K1 launch, out_host[8] ns. */
+int fate_k1_profile(uint64_t *out_host);
+
 /* ---- K4 prefill grouped expert FFN (replaces pipeline.py:733-750) ----------
  * For T tokens X[T,H] (fp32 on device), n experts: token lists tok_idx
  * (concatenated, device int32) with per-expert offsets off[n+1] (host) and

@@ -82,6 +82,8 @@ SIGNATURES = {
     "fate_expert_buffer_bytes": (c_i64, [c_int, c_int, c_int]),
     "fate_gate_forward": (c_int, [c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp]),
     "fate_ffn_decode": (c_int, [c_vp, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_vp, c_vp]),
+    "fate_k3_profile": (c_int, [c_vp]),
+    "fate_k1_profile": (c_int, [c_vp]),
     "fate_ffn_prefill": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), c_vp, c_vp, P_i32, c_vp, c_vp]),
     "fate_engine_create": (c_int, [C.POINTER(EngineConfig), C.POINTER(c_vp)]),
     "fate_engine_destroy": (c_int, [c_vp]),

@@ -16,9 +16,9 @@ struct WarpArc {
   __device__ void load(const ArcLayer *g, ArcLayer *sm) {
     s = sm;
     const int lane = threadIdx.x & 31;
-    const int *src = reinterpret_cast<const int *>(g);
-    int *dst = reinterpret_cast<int *>(sm);
-    for (int i = lane; i < (int)(sizeof(ArcLayer) / 4); i += 32) dst[i] = src[i];
+    const int4 *src = reinterpret_cast<const int4 *>(g);
+    int4 *dst = reinterpret_cast<int4 *>(sm);
+    for (int i = lane; i < (int)(sizeof(ArcLayer) / 16); i += 32) dst[i] = src[i];
     __syncwarp();
     c = sm->c, n1 = sm->n1, n2 = sm->n2, nb1 = sm->nb1, nb2 = sm->nb2, p = sm->p;
   }
@@ -27,9 +27,9 @@ struct WarpArc {
     const int lane = threadIdx.x & 31;
     if (lane == 0) s->n1 = n1, s->n2 = n2, s->nb1 = nb1, s->nb2 = nb2, s->p = p;
     __syncwarp();
-    const int *src = reinterpret_cast<const int *>(s);
-    int *dst = reinterpret_cast<int *>(g);
-    for (int i = lane; i < (int)(sizeof(ArcLayer) / 4); i += 32) dst[i] = src[i];
+    const int4 *src = reinterpret_cast<const int4 *>(s);
+    int4 *dst = reinterpret_cast<int4 *>(g);
+    for (int i = lane; i < (int)(sizeof(ArcLayer) / 16); i += 32) dst[i] = src[i];
     __syncwarp();
   }
 

@@ -147,236 +147,342 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
   __syncwarp();
 }
 
+// K1 phase timestamps of the last launch (globaltimer ns), diagnostics only:
+// [0] block 0 start, [1] tail start, [2] state staged, [3] routed, [4] split,
+// [5] predicted, [6] message posted
+__device__ unsigned long long g_k1_prof[8];
+
+__device__ __forceinline__ unsigned long long gtime1() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct TailSmem {
   ArcLayer arc;
+  int32_t bof_l[EMAX], pend_l[EMAX], bof_n[EMAX], bbits_l[EMAX];
+  uint32_t pgen_l[EMAX], pdone_l[EMAX];
+  int32_t pred_prev[EMAX];
+  int32_t c_free_top, c_step, c_pred_valid, c_pred_layer, c_pred_n, shared_present;
   double z[2 * EMAX], w[2 * EMAX];
   int32_t ord[2 * EMAX];
   int32_t chosen[KMAX], cbuf[KMAX], csrc[KMAX], chit[KMAX], carr[KMAX];
   int32_t rel[4 * KMAX + 4];
   int32_t is_chosen[EMAX];
+  alignas(16) float xs[4096];  // x = sqrt(H) * gate_in, H <= 4096 (float4-read by write_xlay)
 };
 
 __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, const double *__restrict__ gate_in,
                                                                    const int32_t *__restrict__ trace_chosen,
                                                                    fate_step_log *__restrict__ log, int layer,
-                                                                   volatile uint32_t *ready_host) {
+                                                                   volatile uint32_t *ready_host, int token) {
   __shared__ double red[kGateThreads / 32];
-  __shared__ int is_last;
   __shared__ TailSmem S;
+  __shared__ int32_t tchosen[KMAX];
   const int E = d.E, H = d.H, L = d.L;
-  const int token = *(volatile int32_t *)&d.ctrl->next_token;
   const double *h = gate_in + ((int64_t)token * L + layer) * H;
-  const int row = blockIdx.x;
-  const int lrow = row < E ? layer : layer + 1;
-  const int e_row = row < E ? row : row - E;
-  // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
-  {
-    const double *W = d.W + ((int64_t)lrow * E + e_row) * H;
-    double acc = 0.0;
-    const double2 *W2 = reinterpret_cast<const double2 *>(W);
+  // block 0: the tail (stages state while the others work), blocks
+  // 1..n_rows: router rows, last block: the deferred ARC update
+  const int n_rows = gridDim.x - 2;
+  const int row = blockIdx.x - 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_prof[0] = gtime1();
+  if (blockIdx.x == gridDim.x - 1) {
+    // (1) deferred update_after_layer of the previous step, concurrent with the
+    // router rows (it touches layer l-1's tables and the free stack)
+    if (threadIdx.x < 32 && d.ctrl->prev_valid) apply_prev_update(d, &S.arc, log, S.rel);
+  } else if (blockIdx.x > 0) {
+    // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
+    const int lrow = row < E ? layer : layer + 1;
+    const int e_row = row < E ? row : row - E;
+    const double2 *W2 = reinterpret_cast<const double2 *>(d.W + ((int64_t)lrow * E + e_row) * H);
     const double2 *h2 = reinterpret_cast<const double2 *>(h);
-    for (int i = threadIdx.x; i < H / 2; i += kGateThreads) {
-      const double2 a = __ldg(W2 + i), b = __ldg(h2 + i);
-      acc = fma(a.x, b.x, acc);
-      acc = fma(a.y, b.y, acc);
+    const double tau = d.tau[lrow];
+    constexpr int U = 8;  // H <= 2 * U * kGateThreads: every load issued before the first FMA
+    double2 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = threadIdx.x + u * kGateThreads;
+      if (i < H / 2) a[u] = __ldg(W2 + i), b[u] = __ldg(h2 + i);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = threadIdx.x + u * kGateThreads;
+      if (i < H / 2) {
+        acc = fma(a[u].x, b[u].x, acc);
+        acc = fma(a[u].y, b[u].y, acc);
+      }
+    }
+    for (int i = threadIdx.x + U * kGateThreads; i < H / 2; i += kGateThreads) {
+      const double2 x = __ldg(W2 + i), y = __ldg(h2 + i);
+      acc = fma(x.x, y.x, acc);
+      acc = fma(x.y, y.y, acc);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < kGateThreads / 32; ++w) s += red[w];
-      d.logits[row] = __ddiv_rn(s, d.tau[lrow]);
-      __threadfence();
-      const uint32_t ticket = atomicAdd(&d.ctrl->arrive, 1u);
-      is_last = (ticket == gridDim.x - 1);
+      double sum = 0.0;
+      for (int w = 0; w < kGateThreads / 32; ++w) sum += red[w];
+      d.logits[row] = __ddiv_rn(sum, tau);
     }
-    __syncthreads();
   }
-  if (!is_last) return;
-  __threadfence();
+  if (blockIdx.x > 0) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&d.ctrl->arrive, 1u);
+    }
+    return;
+  }
+  // ================= tail block
   Ctrl &C = *d.ctrl;
   // ---- FFN input x = sqrt(H) * gate_in (fp64 product, fp32 storage)
   const double sH = sqrt((double)H);
-  for (int i = threadIdx.x; i < H; i += kGateThreads) d.x[i] = (float)(sH * h[i]);
-  for (int i = threadIdx.x; i < gridDim.x; i += kGateThreads) S.z[i] = ((volatile double *)d.logits)[i];
-  for (int i = threadIdx.x; i < E; i += kGateThreads) S.is_chosen[i] = 0;
+  for (int i = threadIdx.x; i < H; i += kGateThreads) S.xs[i] = (float)(sH * h[i]);
+  __syncthreads();
+  write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
+  // stage every table the tail reads while the router rows are in flight
+  const int pl = C.prev_valid ? C.prev_layer : -1;  // layer the ARC block is editing
+  for (int i = threadIdx.x; i < E; i += kGateThreads) {
+    S.is_chosen[i] = 0;
+    const int pb = d.pend_buf[layer * E + i];
+    S.pend_l[i] = pb;
+    S.pgen_l[i] = d.pend_gen[layer * E + i];
+    S.pdone_l[i] = pb >= 0 ? ((volatile uint32_t *)d.buf_done)[pb] : 0u;
+    if (pl != layer) {
+      const int bb = d.buf_of[layer * E + i];
+      S.bof_l[i] = bb;
+      S.bbits_l[i] = bb >= 0 ? d.buf_bits[bb] : 0;
+    }
+    if (pl != layer + 1) S.bof_n[i] = layer + 1 < L ? d.buf_of[(layer + 1) * E + i] : 0;
+  }
+  if (threadIdx.x < d.k && trace_chosen) tchosen[threadIdx.x] = trace_chosen[((int64_t)token * L + layer) * d.k + threadIdx.x];
+  if (threadIdx.x == 0) {
+    S.c_step = C.step;
+    S.c_pred_valid = C.pred_valid;
+    S.c_pred_layer = C.pred_layer;
+    S.c_pred_n = C.pred_n;
+    S.shared_present = d.shared && d.shared[layer] ? 1 : 0;
+    // wait for the router rows and the ARC block
+    while (*(volatile uint32_t *)&C.arrive < (uint32_t)(gridDim.x - 1)) {
+    }
+    __threadfence();
+    g_k1_prof[1] = gtime1();
+    S.c_free_top = *(volatile int32_t *)&C.free_top;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_rows; i += kGateThreads) S.z[i] = ((volatile double *)d.logits)[i];
+  for (int i = threadIdx.x; i < E; i += kGateThreads) {
+    if (pl == layer) {
+      const int bb = ((volatile int32_t *)d.buf_of)[layer * E + i];
+      S.bof_l[i] = bb;
+      S.bbits_l[i] = bb >= 0 ? ((volatile int32_t *)d.buf_bits)[bb] : 0;
+    }
+    if (pl == layer + 1 && layer + 1 < L) S.bof_n[i] = ((volatile int32_t *)d.buf_of)[(layer + 1) * E + i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < S.c_pred_n; i += kGateThreads) S.pred_prev[i] = C.pred_list[i];
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   if (lane == 0) C.arrive = 0;
   const int k = d.k;
-  const int step = C.step;
+  const int step = S.c_step;
   fate_step_log *lg = log ? log + step : nullptr;
-  // (1) deferred ARC update of the previous step
-  if (C.prev_valid) apply_prev_update(d, &S.arc, log, S.rel);
+  if (lane == 0) g_k1_prof[2] = gtime1();
   // (2) routing of layer l: softmax + rank (gatesim.py:113-123, core.py:159-163)
   warp_softmax_rank(S.z, S.w, S.ord, E, k, 0, d.q);
-  if (lane == 0) {
-    for (int i = 0; i < k; ++i) S.chosen[i] = S.ord[i];
-    for (int i = 1; i < k; ++i)  // ascending ids (pipeline.py:441 iterates sorted(chosen))
-      for (int j = i; j > 0 && S.chosen[j - 1] > S.chosen[j]; --j) {
-        const int t = S.chosen[j];
-        S.chosen[j] = S.chosen[j - 1];
-        S.chosen[j - 1] = t;
-      }
-    for (int i = 0; i < k; ++i) S.is_chosen[S.chosen[i]] = 1;
-    int mism = 0;
-    if (trace_chosen) {
-      const int32_t *tc = trace_chosen + ((int64_t)token * L + layer) * k;
-      for (int i = 0; i < k; ++i) mism |= (tc[i] != S.chosen[i]);
-    }
-    if (mism) atomicAdd(&d.stats->mismatches, 1ull);
-    if (k < E && S.w[S.ord[k - 1]] - S.w[S.ord[k]] < 1e-12) atomicAdd(&d.stats->near_ties, 1ull);
-    if (lg) lg->mismatch = mism;
-    // recall of the prediction made one step earlier (pipeline.py:433-436)
-    if (C.pred_valid && C.pred_layer == layer) {
-      int inter = 0;
-      for (int i = 0; i < C.pred_n; ++i) inter += S.is_chosen[C.pred_list[i]];
-      d.stats->recall_sum += (double)inter / (double)k;
-      d.stats->recall_n += 1;
-      C.pred_valid = 0;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  // chosen ids in ascending order (pipeline.py:441 iterates sorted(chosen)):
+  // lane i < k owns ord[i]; its position = #{j < k : ord[j] < ord[i]}
+  {
+    const int mine = lane < k ? S.ord[lane] : 0x7fffffff;
+    int pos = 0;
+    for (int j = 0; j < k; ++j) pos += __shfl_sync(FULL, mine, j) < mine;
+    if (lane < k) {
+      S.chosen[pos] = mine;
+      S.is_chosen[mine] = 1;
     }
   }
   __syncwarp();
-  // (3) hit / prefetched / on-demand split (pipeline.py:441-459)
+  const bool act = lane < k;
+  const int ce = act ? S.chosen[lane] : 0;
+  {
+    int mism = 0;
+    if (trace_chosen && act) mism = tchosen[lane] != ce;
+    mism = __any_sync(FULL, mism);
+    // recall of the prediction made one step earlier (pipeline.py:433-436)
+    const bool chk = S.c_pred_valid && S.c_pred_layer == layer;
+    int inter = 0;
+    if (chk)
+      for (int i = lane; i < S.c_pred_n; i += 32) inter += S.is_chosen[S.pred_prev[i]];
+    for (int o = 16; o; o >>= 1) inter += __shfl_xor_sync(FULL, inter, o);
+    if (lane == 0) {
+      if (mism) atomicAdd(&d.stats->mismatches, 1ull);
+      if (k < E && S.w[S.ord[k - 1]] - S.w[S.ord[k]] < 1e-12) atomicAdd(&d.stats->near_ties, 1ull);
+      if (lg) lg->mismatch = mism;
+      if (chk) {
+        atomicAdd(&d.stats->recall_sum, (double)inter / (double)k);
+        atomicAdd(&d.stats->recall_n, 1ull);
+        C.pred_valid = 0;
+      }
+    }
+  }
+  if (lane == 0) g_k1_prof[3] = gtime1();
+  // (3) hit / prefetched / on-demand split (pipeline.py:441-459), one lane per chosen expert
   StepMsg *msg = d.ring + (step % kRing);
+  int top = S.c_free_top;
+  const int slot_b = act ? S.bof_l[ce] : -1;
+  const int pend_b = act && slot_b < 0 ? S.pend_l[ce] : -1;
+  const bool hit = act && slot_b >= 0;
+  const bool pref = act && !hit && pend_b >= 0;
+  const bool odm = act && !hit && !pref;
+  const unsigned m_od = __ballot_sync(FULL, odm), m_need = __ballot_sync(FULL, pref);
+  const int n_od = __popc(m_od), n_need = __popc(m_need), i_od = __popc(m_od & lt), i_need = __popc(m_need & lt);
+  int arr = 0, b = slot_b, src = 16;
+  if (hit) src = d.cached_bits < 16 ? d.cached_bits : 16;
+  if (pref) {
+    b = pend_b;
+    src = d.prefetch_bits;
+    arr = S.pdone_l[ce] == S.pgen_l[ce];
+    msg->need_e[i_need] = ce;
+    msg->need_b[i_need] = b;
+  }
+  if (odm) {
+    // pop n_od buffers off the free stack: the first od takes the top
+    b = d.free_stack[top - 1 - i_od];
+    const uint32_t g = d.buf_gen[b] + 1u;
+    d.buf_gen[b] = g;
+    src = d.ondemand_bits;
+    d.buf_bits[b] = d.ondemand_bits;
+    msg->od_e[i_od] = ce;
+    msg->od_b[i_od] = b;
+    msg->od_g[i_od] = g;
+    if (lg) lg->ondemand[i_od] = ce;
+  }
+  top -= n_od;
+  const bool all_landed = __all_sync(FULL, !act || hit || (pref && arr));
+  if (act) {
+    C.prev_chosen[lane] = ce;
+    C.prev_buf[lane] = b;
+    S.cbuf[lane] = b;
+    if (lg) {
+      lg->chosen[lane] = ce;
+      lg->src_bits[lane] = src;
+      lg->hit[lane] = hit;
+      lg->arrived[lane] = arr;
+      lg->routing[lane] = (float)S.w[ce];
+      lg->fmt_bits[lane] = hit ? S.bbits_l[ce] : src;
+    }
+  }
+  const int n_hit = __popc(__ballot_sync(FULL, hit)), n_arr = __popc(__ballot_sync(FULL, arr != 0));
+  const int n_deq = __popc(__ballot_sync(FULL, act && src < 16));
+  // (4) prefetched-but-not-chosen experts of this layer: release their buffers
+  // and tell the host to drop them if still queued (drop_stale, pipeline.py:438/247-253)
+  int n_drop = 0;
+  for (int base = 0; base < E; base += 32) {
+    const int e = base + lane;
+    const int pb = e < E ? S.pend_l[e] : -1;
+    if (pb >= 0) d.pend_buf[layer * E + e] = -1;
+    const bool drop = pb >= 0 && !S.is_chosen[e];
+    const unsigned m = __ballot_sync(FULL, drop);
+    if (drop) {
+      const int i = n_drop + __popc(m & lt);
+      msg->drop_e[i] = e;
+      msg->drop_b[i] = pb;
+      d.free_stack[top + __popc(m & lt)] = pb;
+    }
+    top += __popc(m);
+    n_drop += __popc(m);
+  }
+  if (lane == 0) g_k1_prof[4] = gtime1();
+  // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
+  int n_pf = 0, n_pred = -1;
+  if (d.use_predictor && layer + 1 < L) {
+    const int len = warp_softmax_rank(S.z + E, S.w + E, S.ord + E, E, k, d.policy, d.q);
+    n_pred = len < d.budget_n ? len : d.budget_n;
+    for (int base = 0; base < n_pred; base += 32) {
+      const int i = base + lane;
+      const int e = i < n_pred ? S.ord[E + i] : 0;
+      if (i < n_pred) {
+        C.pred_list[i] = e;
+        if (lg) lg->pred[i] = e;
+      }
+      const bool issue = i < n_pred && S.bof_n[e] < 0;  // resident: skip (pipeline.py:397)
+      const unsigned m = __ballot_sync(FULL, issue);
+      if (issue) {
+        const int j = n_pf + __popc(m & lt);
+        const int nb = d.free_stack[top - 1 - __popc(m & lt)];
+        const uint32_t g = d.buf_gen[nb] + 1u;
+        d.buf_gen[nb] = g;
+        d.buf_bits[nb] = d.prefetch_bits;
+        d.pend_buf[(layer + 1) * E + e] = nb;
+        d.pend_gen[(layer + 1) * E + e] = g;
+        msg->pf_e[j] = e;
+        msg->pf_b[j] = nb;
+        msg->pf_g[j] = g;
+        msg->pf_bits_each[j] = d.prefetch_bits;
+        if (lg) lg->prefetch[j] = e;
+      }
+      top -= __popc(m);
+      n_pf += __popc(m);
+    }
+  }
+  __syncwarp();
   if (lane == 0) {
-    int n_od = 0, n_need = 0, n_hit = 0, n_arr = 0, n_deq = 0;
-    bool all_landed = true;
-    for (int i = 0; i < k; ++i) {
-      const int e = S.chosen[i];
-      int b = d.buf_of[layer * E + e];
-      int src, hit = 0, arr = 0;
-      if (b >= 0) {
-        hit = 1;
-        src = d.cached_bits < 16 ? d.cached_bits : 16;
-      } else if (d.pend_buf[layer * E + e] >= 0) {
-        b = d.pend_buf[layer * E + e];
-        src = d.prefetch_bits;
-        arr = ((volatile uint32_t *)d.buf_done)[b] == d.pend_gen[layer * E + e];
-        all_landed = all_landed && arr;
-        msg->need_e[n_need] = e;
-        msg->need_b[n_need] = b;
-        ++n_need;
-      } else {
-        b = pop_free(d);
-        const uint32_t g = ++d.buf_gen[b];
-        src = d.ondemand_bits;
-        d.buf_bits[b] = d.ondemand_bits;
-        msg->od_e[n_od] = e;
-        msg->od_b[n_od] = b;
-        msg->od_g[n_od] = g;
-        if (lg) lg->ondemand[n_od] = e;
-        ++n_od;
-        all_landed = false;
-      }
-      C.prev_chosen[i] = e;
-      C.prev_buf[i] = b;
-      S.cbuf[i] = b;
-      n_hit += hit;
-      n_arr += arr;
-      n_deq += src < 16;
-      if (lg) {
-        lg->chosen[i] = e;
-        lg->src_bits[i] = src;
-        lg->hit[i] = hit;
-        lg->arrived[i] = arr;
-        lg->routing[i] = (float)S.w[e];
-        lg->fmt_bits[i] = d.buf_bits[b];
-      }
+    if (top < 0 || top > d.nbuf) C.err = 1;
+    C.free_top = top;
+    if (n_pred >= 0) {
+      C.pred_n = n_pred;
+      C.pred_layer = layer + 1;
+      C.pred_valid = 1;
     }
-    // (4) prefetched-but-not-chosen experts of this layer: release their buffers
-    // and tell the host to drop them if still queued (drop_stale, pipeline.py:438/247-253)
-    int n_drop = 0;
-    for (int e = 0; e < E; ++e) {
-      const int b = d.pend_buf[layer * E + e];
-      if (b < 0) continue;
-      d.pend_buf[layer * E + e] = -1;
-      if (S.is_chosen[e]) continue;
-      msg->drop_e[n_drop] = e;
-      msg->drop_b[n_drop] = b;
-      ++n_drop;
-      push_free(d, b);
-    }
-    msg->n_od = n_od;
-    msg->n_need = n_need;
-    msg->n_drop = n_drop;
-    msg->od_bits = d.ondemand_bits;
-    msg->pf_bits = d.prefetch_bits;
-    if (lg) lg->n_ondemand = n_od;
+    if (lg) lg->n_pred = n_pred, lg->n_prefetch = n_pf, lg->n_ondemand = n_od;
     atomicAdd(&d.stats->accesses, (unsigned long long)k);
     atomicAdd(&d.stats->cache_hits, (unsigned long long)n_hit);
     atomicAdd(&d.stats->arrival_hits, (unsigned long long)n_arr);
     atomicAdd(&d.stats->dequant_count, (unsigned long long)n_deq);
     atomicAdd(&d.stats->ondemand_issued, (unsigned long long)n_od);
-    S.carr[0] = all_landed ? 1 : 0;
+    atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
   }
-  __syncwarp();
-  // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
-  int n_pf = 0;
-  if (d.use_predictor && layer + 1 < L) {
-    const int len = warp_softmax_rank(S.z + E, S.w + E, S.ord + E, E, k, d.policy, d.q);
-    if (lane == 0) {
-      const int n = len < d.budget_n ? len : d.budget_n;
-      C.pred_n = n;
-      C.pred_layer = layer + 1;
-      C.pred_valid = 1;
-      for (int i = 0; i < n; ++i) {
-        const int e = S.ord[E + i];
-        C.pred_list[i] = e;
-        if (lg) lg->pred[i] = e;
-        if (d.buf_of[(layer + 1) * E + e] >= 0) continue;  // resident: skip (pipeline.py:397)
-        const int b = pop_free(d);
-        const uint32_t g = ++d.buf_gen[b];
-        d.buf_bits[b] = d.prefetch_bits;
-        d.pend_buf[(layer + 1) * E + e] = b;
-        d.pend_gen[(layer + 1) * E + e] = g;
-        msg->pf_e[n_pf] = e;
-        msg->pf_b[n_pf] = b;
-        msg->pf_g[n_pf] = g;
-        msg->pf_bits_each[n_pf] = d.prefetch_bits;
-        if (lg) lg->prefetch[n_pf] = e;
-        ++n_pf;
-      }
-      if (lg) lg->n_pred = n, lg->n_prefetch = n_pf;
-      atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
-    }
-  } else if (lane == 0 && lg) {
-    lg->n_pred = -1;
-    lg->n_prefetch = 0;
-  }
-  __syncwarp();
+  if (lane == 0) g_k1_prof[5] = gtime1();
   // (6) the K3 batch: routed experts weighted by their full-softmax routing
   // weight (not renormalised), plus the shared expert with weight 1.
+  // storage width of every buffer is known here (hit: the slot's tagged width;
+  // fetched: the width requested), so K3 never reads headers on its critical path
+  FfnBatch &B = *d.batch;
+  if (act)
+    B.e[lane] = FfnExpert{d.pool + (int64_t)b * d.buf_stride, (float)S.w[ce], d.I, hit ? S.bbits_l[ce] : src,
+                          lane * d.I};
   if (lane == 0) {
-    FfnBatch &B = *d.batch;
-    B.H = H;
-    int off = 0, n = 0;
-    for (int i = 0; i < k; ++i) {
-      B.e[n] = FfnExpert{d.pool + (int64_t)S.cbuf[i] * d.buf_stride, (float)S.w[S.chosen[i]], d.I, 0, off};
-      off += d.I;
-      ++n;
-    }
-    if (d.shared && d.shared[layer]) {
-      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, 0, off};
+    int n = k, off = k * d.I;
+    if (S.shared_present) {
+      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, d.shared_bits, off};
       off += d.I_shared;
       ++n;
     }
+    B.H = H;
     B.n = n;
     B.total_I = off;
     // (7) step message + (8) self-signal when nothing must be waited for
+    msg->n_od = n_od;
+    msg->n_need = n_need;
+    msg->n_drop = n_drop;
     msg->n_pf = n_pf;
+    msg->od_bits = d.ondemand_bits;
+    msg->pf_bits = d.prefetch_bits;
     msg->step = step;
     msg->token = token;
     msg->layer = layer;
-    const int self = S.carr[0];
-    msg->self_signaled = self;
-    if (self) ready_host[layer] = (uint32_t)token + 1u;
-    __threadfence_system();
+    msg->self_signaled = all_landed ? 1 : 0;
+    if (all_landed) ready_host[layer] = (uint32_t)token + 1u;
+  }
+  __syncwarp();
+  __threadfence_system();
+  if (lane == 0) {
     msg->seq = (uint32_t)step + 1u;
-    __threadfence_system();
     // (9) control block for the next step
     C.prev_valid = 1;
     C.prev_layer = layer;
@@ -386,6 +492,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     C.cur_layer = layer;
     C.step = step + 1;
     if (layer == L - 1) C.next_token = token + 1;
+    g_k1_prof[6] = gtime1();
     __threadfence();
   }
 }
@@ -569,7 +676,7 @@ int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 int check_cfg(const fate_engine_config *c) {
   if (!c || c->num_layers < 1 || c->num_experts < 1 || c->num_experts > FATE_MAX_EXPERTS || c->top_k < 1 ||
-      c->top_k > c->num_experts || c->top_k > FATE_MAX_TOPK || c->hidden_dim < 64 || c->hidden_dim % 64 ||
+      c->top_k > c->num_experts || c->top_k > FATE_MAX_TOPK || c->hidden_dim < 64 || c->hidden_dim > 4096 || c->hidden_dim % 64 ||
       c->intermediate_dim < 64 || c->intermediate_dim % 64 || c->shared_intermediate < 0 ||
       c->shared_intermediate % 64 || !c->capacity || c->budget_n < 0 || c->max_tokens < 1) {
     set_error("fate_engine_create: invalid geometry");
@@ -615,6 +722,14 @@ int copy_to_buffers(fate_engine *g, const int32_t *loads_dev, int layer, int bit
 }  // namespace
 
 static int prefill_preload();
+
+extern "C" int fate_k1_profile(uint64_t *out_host) {
+  if (cudaMemcpyFromSymbol(out_host, g_k1_prof, sizeof(unsigned long long) * 8) != cudaSuccess) {
+    set_error("fate_k1_profile: copy failed");
+    return FATE_ECUDA;
+  }
+  return FATE_OK;
+}
 
 extern "C" int fate_version(void) { return 1; }
 extern "C" const char *fate_last_error(void) { return g_err.c_str(); }
@@ -680,9 +795,9 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
                o_fs = carve((size_t)nbuf * 4), o_bg = carve((size_t)nbuf * 4), o_bd = carve((size_t)nbuf * 4),
                o_bb = carve((size_t)nbuf * 4),
                o_ctrl = carve(sizeof(Ctrl)), o_st = carve(sizeof(DevStats)), o_lg = carve(2 * EMAX * 8),
-               o_x = carve((size_t)std::max(H, 4096) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
+               o_x = carve(ffn_xlay_floats(H) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
                o_sh = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
-               o_a = carve((size_t)g->max_total_I * 4);
+               o_a = carve(ffn_alay_floats(g->max_total_I) * 4);
   FATE_CUDA(cudaMalloc(&g->dev_block, off));
   FATE_CUDA(cudaMemset(g->dev_block, 0, off));
   uint8_t *base = (uint8_t *)g->dev_block;
@@ -1019,10 +1134,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     // enqueue compute for steps up to `lookahead` beyond the host's progress
     while (launched < n_steps && launched < processed + lookahead) {
       const int s = launched, t = s / L, l = s % L;
-      const int rows = (rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts;
+      // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
+      const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
       decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
-                                                        (volatile uint32_t *)g->ready_dev);
+                                                        (volatile uint32_t *)g->ready_dev, t);
       FATE_CHECK_LAUNCH("decode_gate_kernel");
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
@@ -1087,6 +1203,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     if ((status = ch.pump())) break;
     if (m.seq != (uint32_t)processed + 1u) {
       _mm_pause();
+      const cudaError_t qe = cudaStreamQuery(cs);
+      if (qe != cudaSuccess && qe != cudaErrorNotReady) {
+        status = cuda_status(qe, "decode compute stream (device fault)");
+        break;
+      }
       if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(30)) {
         // watchdog: release the compute stream so the GPU is never left hung
         for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
@@ -1530,6 +1651,9 @@ __global__ void prefill_arc_kernel(EngineDev d, PfScratch s, int layer, int n_ac
       if (!hit) {
         const int b = s.stage[e];
         if (arc.c >= 1) {
+          // the slot keeps the width that actually landed (a prefetch the host
+          // re-issued as an on-demand load carries the narrower header)
+          d.buf_bits[b] = reinterpret_cast<const ExpertHeader *>(d.pool + (int64_t)b * d.buf_stride)->bits;
           d.buf_of[layer * d.E + e] = b;
           for (int r = 0; r < nrel; ++r)
             if (rel[r] == b) rel[r] = rel[--nrel], r = nrel;

@@ -10,7 +10,7 @@ constexpr int EMAX = FATE_MAX_EXPERTS;
 constexpr int KMAX = FATE_MAX_TOPK;
 
 // One layer's ARC lists (cache.py:104-179), LRU first.
-struct ArcLayer {
+struct alignas(16) ArcLayer {
   int32_t c, n1, n2, nb1, nb2, pad0;
   double p;
   int32_t t1[EMAX], t2[EMAX], b1[EMAX], b2[EMAX];
@@ -82,7 +82,7 @@ struct EngineDev {
   Ctrl *ctrl;
   DevStats *stats;
   double *logits;             // [2E]
-  float *x;                   // [H]
+  float *x;                   // x in the four chunk-transposed K3 layouts (write_xlay)
   FfnBatch *batch;
   StepMsg *ring;              // mapped pinned [kRing]
 };

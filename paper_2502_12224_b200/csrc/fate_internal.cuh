@@ -108,13 +108,39 @@ struct FfnBatch {
   FfnExpert e[kMaxFfnExperts];
 };
 
-// Launch the two K3 phases for a batch described in DEVICE memory (`batch`),
-// with upper bounds known on the host (for graph-stable grids).
-cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *x_dev, float *a_dev, float *y_dev,
-                              int H, int max_total_I, cudaStream_t s);
-
-cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *x_dev, float *a_dev, float *y_dev,
+// K3 launch (one kernel per step).  xlay: x in every chunk-transposed width
+// layout (ffn_xlay_floats(H) floats, see write_xlay); alay: activation layout
+// scratch (ffn_alay_floats(max_total_I) floats).  The batch is in DEVICE memory.
+cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
+                              int max_total_I, cudaStream_t s);
+cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev,
                                      int H, int max_total_I, unsigned long long *bytes_stat, cudaStream_t s);
+cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s);
+size_t ffn_xlay_floats(int H);
+size_t ffn_alay_floats(int max_total_I);
+
+// x (in shared memory) -> the four chunk-transposed layouts + chunk sums, by
+// a whole thread block: slot s (chunk width 8 << s) at xlay + s*(H/4 + H/32) float4.
+__device__ inline void write_xlay(const float *x, int H, float4 *xlay, int tid, int nthr) {
+  const int stride = H / 4 + H / 32;
+  for (int sl = 0; sl < 4; ++sl) {
+    const int cols = 8 << sl, nch = H / cols, nq = cols / 4;
+    float4 *xt = xlay + sl * stride;
+    float *sums = reinterpret_cast<float *>(xt + H / 4);
+    for (int i = tid; i < H / 4; i += nthr) {
+      const int c = (4 * i) / cols, m = ((4 * i) % cols) / 4;
+      xt[m * nch + c] = reinterpret_cast<const float4 *>(x)[i];
+    }
+    for (int c = tid; c < nch; c += nthr) {
+      float acc = 0.f;
+      for (int m = 0; m < nq; ++m) {
+        const float4 q = reinterpret_cast<const float4 *>(x)[(c * cols) / 4 + m];
+        acc += (q.x + q.y) + (q.z + q.w);
+      }
+      sums[c] = acc;
+    }
+  }
+}
 
 cudaError_t ffn_preload();
 

@@ -55,6 +55,7 @@ __device__ inline int warp_softmax_rank(const double *z, double *w, int32_t *ord
   for (int e = lane; e < E; e += 32) {
     const double we = w[e];
     int r = 0;
+#pragma unroll 8
     for (int j = 0; j < E; ++j) {
       const double wj = w[j];
       r += (wj > we) || (wj == we && j < e);

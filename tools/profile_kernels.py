@@ -1,0 +1,106 @@
+"""Kernel-level measurement harness (not a bench line).
+
+  k3      : K3 (ffn_up + ffn_down) standalone at the Qwen decode shape: 4 routed
+            INT4 experts + the bf16 shared expert (5632), rotating over 24
+            expert sets so the working set (~2 GB) exceeds L2; CUDA-event timed.
+  allhit  : the decode engine on the Qwen shape with every expert resident
+            (capacity = E in every layer), so no step waits on the host; used
+            for ncu captures of K1/K3 inside the real step sequence.
+Usage: python tools/profile_kernels.py k3|allhit [iters]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2502_12224_b200 import ops  # noqa: E402
+
+
+def k3(iters: int):
+    H, I, Is = 2048, 1408, 5632
+    g = torch.Generator(device="cuda").manual_seed(0)
+    sets = []
+    for s in range(24):
+        bufs = []
+        for j in range(4):
+            w = [torch.randn(sh, generator=g, device="cuda") * 0.02 for sh in ((I, H), (I, H), (H, I))]
+            bufs.append(ops.pack_expert(*w, 4 if j != 3 else 2))
+        w = [torch.randn(sh, generator=g, device="cuda") * 0.02 for sh in ((Is, H), (Is, H), (H, Is))]
+        bufs.append(ops.pack_expert(*w, 16))
+        sets.append(bufs)
+    x = torch.randn(H, device="cuda")
+    nbytes = [sum(b.numel() - 256 for b in s) for s in sets]
+    for s in sets[:4]:
+        ops.ffn_decode(x, s, [0.3, 0.2, 0.1, 0.05, 1.0])
+    torch.cuda.synchronize()
+    # the standalone entry point synchronizes per call; time the device span with events
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for i in range(iters):
+        s = sets[i % len(sets)]
+        ev[i][0].record()
+        ops.ffn_decode(x, s, [0.3, 0.2, 0.1, 0.05, 1.0])
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(b) for a, b in ev])
+    by = np.array([nbytes[i % len(sets)] for i in range(iters)])
+    out = {"k3_ms_median": float(np.median(ms)), "bytes": int(by[0]), "gbs_median": float(np.median(by / (ms * 1e-3)) / 1e9)}
+    print(json.dumps(out))
+
+
+def allhit(iters: int):
+    from paper_2502_12224_b200.core import ModelConfig
+    from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
+    from paper_2502_12224_b200.experts import ExpertStore
+    from paper_2502_12224_b200.gatesim import GenConfig, gen_trace
+    cfg = ModelConfig.from_shape(24, 60, 4, 2048, 1408, 3)
+    tr, w = gen_trace(cfg, GenConfig(seed=0, num_tokens=iters))
+    store = ExpertStore(cfg, bits=(4, 2), shared_intermediate=5632, shared_bits=16)
+    eng = OffloadEngine(cfg, [60] * 24, store, w, StrategyKnobs(budget_n=0), max_tokens=max(iters, 64))
+    for l in range(24):
+        eng.seed_resident(l, range(60))
+    _, g, ch = tr.dense_arrays(cfg)
+    gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
+    eng.decode(gd[:4], chd[:4])
+    t0 = time.perf_counter()
+    res = eng.decode(gd, chd)
+    wall = time.perf_counter() - t0
+    st = res.stats
+    from paper_2502_12224_b200 import _lib
+    buf = np.zeros(160 * 8 + 64 * 3, dtype=np.uint64)
+    _lib.load().fate_k3_profile(buf.ctypes.data)
+    prof = buf[:1280].reshape(160, 8)
+    tiles = buf[1280:].reshape(64, 3).astype(np.float64)
+    P = prof[:148].astype(np.float64)
+    t0 = P[:, 0].min()
+    rel = (P - t0) / 1000.0
+    names = ["start", "cons", "xlay", "phaseA", "gbar", "alay", "phaseB", "prod_done"]
+    print("K3 phase timestamps (us from first CTA start): median / max over CTAs")
+    for i, nm in enumerate(names):
+        print(f"  {nm:10s} {np.median(rel[:, i]):8.2f} {rel[:, i].max():8.2f}")
+    t00 = P[0, 0]
+    print("CTA0 tiles (us): issue / full seen (warp0) / released (warp0)")
+    for i in range(64):
+        if tiles[i, 0] == 0 and tiles[i, 1] == 0:
+            break
+        print(f"  {i:3d} {(tiles[i,0]-t00)/1e3:8.2f} {(tiles[i,1]-t00)/1e3:8.2f} {(tiles[i,2]-t00)/1e3:8.2f}")
+    k1 = np.zeros(8, dtype=np.uint64)
+    _lib.load().fate_k1_profile(k1.ctypes.data)
+    k1 = (k1.astype(np.float64) - float(k1[0])) / 1000.0
+    print("K1 phases (us): tail_start %.2f staged %.2f routed %.2f split %.2f predicted %.2f posted %.2f" %
+          tuple(k1[1:7]))
+    print(json.dumps({"tokens": iters, "gpu_ms": st["gpu_ms"], "tok_s": iters / st["gpu_ms"] * 1e3, "wall_s": wall,
+                      "k3_ms": st["ffn_ms"] / st["steps"], "k1_ms": st["gate_ms"] / st["steps"],
+                      "k3_gbs": st["ffn_bytes"] / st["steps"] / (st["ffn_ms"] / st["steps"] * 1e-3) / 1e9,
+                      "hits": st["cache_hits"], "accesses": st["accesses"]}))
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1]
+    it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+    {"k3": k3, "allhit": allhit}[mode](it)
