@@ -99,9 +99,20 @@ int fate_gate_forward(const double *W_dev, double tau, const double *h_dev, int 
 int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *const *bufs, const float *weights,
                     float *scratch_dev, float *y_dev, void *stream);
 
+/* Measurement: K3 launched `iters` times back to back on `stream`, cycling
+ * over `nsets` expert sets (bufs[nsets*n], set q = bufs[q*n .. q*n+n)) so the
+ * working set can exceed L2; batches and layouts are built once; *ms_out =
+ * mean kernel time in ms from CUDA events around the launches. */
+int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets, const uint8_t *const *bufs,
+                          const float *weights, float *y_dev, int iters, void *stream, float *ms_out);
+
 /* Diagnostics: per-CTA phase timestamps (globaltimer ns) of the last K3
  * launch, out_host[160*8]: start, consumers start, x layouts done, phase A
- * done, grid barrier passed, activation layouts done, phase B done, producer done. */
+ * done, grid barrier passed, activation layouts done, phase B done, producer
+ * done; then out_host[160*8 + 17*48*3]: CTA 0 per-warp tile trace in SM
+ * cycles, [warp][tile][3] (producer: empty-wait start, empty passed, issued;
+ * consumers: full-wait start, full passed, released); then [8][4] cycles of
+ * consumer warp 1's first phase-A rows (dots done, sums done, store done). */
 int fate_k3_profile(uint64_t *out_host);
 /* Diagnostics: phase timestamps of the last K1 launch, out_host[8] ns. */
 int fate_k1_profile(uint64_t *out_host);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "fate_gate_forward": (c_int, [c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp]),
     "fate_ffn_decode": (c_int, [c_vp, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_vp, c_vp]),
     "fate_k3_profile": (c_int, [c_vp]),
+    "fate_ffn_decode_timed": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_int,
+                                      c_vp, C.POINTER(C.c_float)]),
     "fate_k1_profile": (c_int, [c_vp]),
     "fate_ffn_prefill": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), c_vp, c_vp, P_i32, c_vp, c_vp]),
     "fate_engine_create": (c_int, [C.POINTER(EngineConfig), C.POINTER(c_vp)]),

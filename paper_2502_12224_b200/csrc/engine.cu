@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     B.H = H;
     B.n = n;
     B.total_I = off;
+    B.work = 0u;
     // (7) step message + (8) self-signal when nothing must be waited for
     msg->n_od = n_od;
     msg->n_need = n_need;
@@ -676,9 +677,9 @@ int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 int check_cfg(const fate_engine_config *c) {
   if (!c || c->num_layers < 1 || c->num_experts < 1 || c->num_experts > FATE_MAX_EXPERTS || c->top_k < 1 ||
-      c->top_k > c->num_experts || c->top_k > FATE_MAX_TOPK || c->hidden_dim < 64 || c->hidden_dim > 4096 || c->hidden_dim % 64 ||
-      c->intermediate_dim < 64 || c->intermediate_dim % 64 || c->shared_intermediate < 0 ||
-      c->shared_intermediate % 64 || !c->capacity || c->budget_n < 0 || c->max_tokens < 1) {
+      c->top_k > c->num_experts || c->top_k > FATE_MAX_TOPK || c->hidden_dim < 128 || c->hidden_dim > 4096 || c->hidden_dim % 128 ||
+      c->intermediate_dim < 128 || c->intermediate_dim % 128 || c->shared_intermediate < 0 ||
+      c->shared_intermediate % 128 || !c->capacity || c->budget_n < 0 || c->max_tokens < 1) {
     set_error("fate_engine_create: invalid geometry");
     return FATE_EINVAL;
   }

@@ -105,8 +105,10 @@ struct FfnBatch {
   int n;
   int H;
   int total_I;
+  unsigned int work;   // K3 phase-A tile counter (dynamic scheduling); zero before each launch
   FfnExpert e[kMaxFfnExperts];
 };
+static_assert(sizeof(FfnBatch) % 16 == 0, "K3 copies the batch with 16-byte loads");
 
 // K3 launch (one kernel per step).  xlay: x in every chunk-transposed width
 // layout (ffn_xlay_floats(H) floats, see write_xlay); alay: activation layout

@@ -22,15 +22,19 @@
 //    FFMA per weight element plus code extraction.
 #include <cuda_bf16.h>
 
+#include <vector>
+
 #include "fate_internal.cuh"
 
 namespace fate {
 namespace {
 
-constexpr int kConsumers = 16;
+constexpr int kConsumers = 12;  // 13 warps -> 128 registers per thread (allocation in 4-warp units)
 constexpr int kThreads = 32 * (1 + kConsumers);
 constexpr int kStageBytes = 32 * 1024;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 6;
+constexpr int kSubRows = 16;     // phase B rows per sub-block (r = 4m + warp%4, m < 4)
+constexpr int kMaxBChunks = 96;  // phase B 16-byte chunks per row per tile (3 groups of 32 lanes)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxUpRows = 64;
 
@@ -77,18 +81,20 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the con
 // ---------------------------------------------------------------------------
 // arithmetic on one 16-byte chunk
 
-// Exact small-integer to float: 2^23 + c has c in the low mantissa bits.
-__device__ __forceinline__ float code_f(uint32_t word, int sh, uint32_t mask) {
-  return __int_as_float(0x4B000000u | ((word >> sh) & mask)) - 8388608.0f;
+// ---------------------------------------------------------------------------
+// code extraction: exact small integers as floats through the 2^23 magic
+// number.  PRMT places one byte of v under the exponent byte 0x4B, so the
+// float is 2^23 + byte exactly; one FSUB2 removes the offset for two codes.
+
+constexpr uint32_t kMagic23 = 0x4B000000u;
+
+template <int K>
+__device__ __forceinline__ float mag(uint32_t v) {
+  return __uint_as_float(__byte_perm(v, kMagic23, 0x7650 + K));
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
-
-template <int BITS>
-struct Fmt {
-  static constexpr int kCols = 128 / BITS;  // columns per 16-byte chunk
-};
 
 // Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2): two weight elements per
 // instruction.  The activation quads are consumed as (x, y) and (z, w) pairs.
@@ -109,92 +115,54 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return *reinterpret_cast<float2 *>(&d);
 }
 
-// two codes (bit offsets sh, sh + BITS) of a word as an exact float pair
-template <int BITS>
-__device__ __forceinline__ float2 codes2(uint32_t w, int sh) {
-  constexpr uint32_t mask = (1u << BITS) - 1u;
-  const float2 m = make_float2(__int_as_float(0x4B000000u | ((w >> sh) & mask)),
-                               __int_as_float(0x4B000000u | ((w >> (sh + BITS)) & mask)));
-  return fsub2(m, make_float2(8388608.0f, 8388608.0f));
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)));
+  return *reinterpret_cast<float2 *>(&d);
 }
 
 __device__ __forceinline__ float2 lo2(const float4 &v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(const float4 &v) { return make_float2(v.z, v.w); }
 
-// Dot of NR rows' 16-byte code chunks (same column chunk c) with the shared
-// activation chunk: each activation quad is loaded once for all NR rows.
-// acc[r] holds two independent FFMA2 chains per row.
-template <int BITS, int NR>
-__device__ __forceinline__ void chunk_dot_rows(const uint4 (&q)[NR], const float4 *__restrict__ xt, int ld, int c,
-                                               float2 (&acc)[NR][2]) {
-  if constexpr (BITS == 16) {
-    const float4 x0 = xt[c], x1 = xt[ld + c];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      acc[r][0] = ffma2(make_float2(bf_lo(q[r].x), bf_hi(q[r].x)), lo2(x0), acc[r][0]);
-      acc[r][1] = ffma2(make_float2(bf_lo(q[r].y), bf_hi(q[r].y)), hi2(x0), acc[r][1]);
-      acc[r][0] = ffma2(make_float2(bf_lo(q[r].z), bf_hi(q[r].z)), lo2(x1), acc[r][0]);
-      acc[r][1] = ffma2(make_float2(bf_lo(q[r].w), bf_hi(q[r].w)), hi2(x1), acc[r][1]);
-    }
-  } else {
-    constexpr int qpw = 32 / BITS / 4;  // activation quads per 32-bit code word
-#pragma unroll
-    for (int wi = 0; wi < 4; ++wi)
-#pragma unroll
-      for (int qi = 0; qi < qpw; ++qi) {
-        const float4 xv = xt[(wi * qpw + qi) * ld + c];
-        const int sh = qi * 4 * BITS;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const uint32_t w = wi == 0 ? q[r].x : wi == 1 ? q[r].y : wi == 2 ? q[r].z : q[r].w;
-          acc[r][0] = ffma2(codes2<BITS>(w, sh), lo2(xv), acc[r][0]);
-          acc[r][1] = ffma2(codes2<BITS>(w, sh + 2 * BITS), hi2(xv), acc[r][1]);
-        }
-      }
-  }
+template <int WI>
+__device__ __forceinline__ uint32_t word(const uint4 &q) {
+  return WI == 0 ? q.x : WI == 1 ? q.y : WI == 2 ? q.z : q.w;
 }
 
-// Partial dots of NR rows held in shared memory (rows at codes[r], scale/zero
-// pairs at sz[r]): chunks c = c_begin + stride*i.  Returns per-row sums.
-template <int BITS, int NR>
-__device__ __forceinline__ void rows_dot_smem(const uint8_t *const (&codes)[NR], const float2 *const (&sz)[NR],
-                                              const float4 *xt, const float *xs, int nch, int c_begin, int c_stride,
-                                              float (&out)[NR]) {
-  float acc_s[NR];
-#pragma unroll
-  for (int r = 0; r < NR; ++r) acc_s[r] = 0.f;
-  for (int c = c_begin; c < nch; c += c_stride) {
-    uint4 q[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) q[r] = reinterpret_cast<const uint4 *>(codes[r])[c];
-    float2 acc[NR][2];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = make_float2(0.f, 0.f);
-    chunk_dot_rows<BITS, NR>(q, xt, nch, c, acc);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const float p = (acc[r][0].x + acc[r][0].y) + (acc[r][1].x + acc[r][1].y);
-      if constexpr (BITS == 16) {
-        acc_s[r] += p;
-      } else {
-        const float2 z = sz[r][c * Fmt<BITS>::kCols / kGroup];
-        acc_s[r] = fmaf(z.x, p, fmaf(z.y, xs[c], acc_s[r]));
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < NR; ++r) out[r] = acc_s[r];
-}
-
-// single-row convenience wrapper
+// One 32-bit code word against its activations xv[0 .. 32/BITS/4): two
+// independent FFMA2 chains.  Element i of a byte sits at bit i*BITS (quant.py:30-39).
 template <int BITS>
-__device__ __forceinline__ float row_dot_smem(const uint8_t *codes, const float2 *sz, const float4 *xt,
-                                              const float *xs, int nch, int c_begin, int c_stride) {
-  const uint8_t *const cs[1] = {codes};
-  const float2 *const zs[1] = {sz};
-  float out[1];
-  rows_dot_smem<BITS, 1>(cs, zs, xt, xs, nch, c_begin, c_stride, out);
-  return out[0];
+__device__ __forceinline__ void word_dot(uint32_t w, const float4 (&xv)[4], float2 &a0, float2 &a1) {
+  const float2 m = make_float2(8388608.0f, 8388608.0f);
+  if constexpr (BITS == 8) {
+    a0 = ffma2(fsub2(make_float2(mag<0>(w), mag<1>(w)), m), lo2(xv[0]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<2>(w), mag<3>(w)), m), hi2(xv[0]), a1);
+  } else if constexpr (BITS == 4) {
+    const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;  // elements 2k | 2k+1 in byte k
+    a0 = ffma2(fsub2(make_float2(mag<0>(lo), mag<0>(hi)), m), lo2(xv[0]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<1>(lo), mag<1>(hi)), m), hi2(xv[0]), a1);
+    a0 = ffma2(fsub2(make_float2(mag<2>(lo), mag<2>(hi)), m), lo2(xv[1]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<3>(lo), mag<3>(hi)), m), hi2(xv[1]), a1);
+  } else {
+    static_assert(BITS == 2, "2/4/8-bit codes");
+    const uint32_t b0 = w & 0x03030303u, b1 = (w >> 2) & 0x03030303u;  // elements 4k+s in byte k of b_s
+    const uint32_t b2 = (w >> 4) & 0x03030303u, b3 = (w >> 6) & 0x03030303u;
+    a0 = ffma2(fsub2(make_float2(mag<0>(b0), mag<0>(b1)), m), lo2(xv[0]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<0>(b2), mag<0>(b3)), m), hi2(xv[0]), a1);
+    a0 = ffma2(fsub2(make_float2(mag<1>(b0), mag<1>(b1)), m), lo2(xv[1]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<1>(b2), mag<1>(b3)), m), hi2(xv[1]), a1);
+    a0 = ffma2(fsub2(make_float2(mag<2>(b0), mag<2>(b1)), m), lo2(xv[2]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<2>(b2), mag<2>(b3)), m), hi2(xv[2]), a1);
+    a0 = ffma2(fsub2(make_float2(mag<3>(b0), mag<3>(b1)), m), lo2(xv[3]), a0);
+    a1 = ffma2(fsub2(make_float2(mag<3>(b2), mag<3>(b3)), m), hi2(xv[3]), a1);
+  }
+}
+
+// bf16 word pair (elements 2u, 2u+1 of a chunk) against an activation pair
+__device__ __forceinline__ float2 bf_dot(uint32_t w, float2 x, float2 acc) {
+  return ffma2(make_float2(bf_lo(w), bf_hi(w)), x, acc);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -204,37 +172,21 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 __device__ __forceinline__ int bits_slot(int bits) { return bits == 16 ? 0 : bits == 8 ? 1 : bits == 4 ? 2 : 3; }
-__device__ __forceinline__ int slot_cols(int slot) { return slot == 0 ? 8 : slot == 1 ? 16 : slot == 2 ? 32 : 64; }
 __host__ __device__ __forceinline__ int64_t sz_row_bytes(int K, int bits) {
   return bits == 16 ? 0 : (int64_t)K / kGroup * 8;
-}
-
-// Copy the batch; experts with bits == 0 take their storage width from the
-// packed buffer's header (a copy that landed in a staging slot carries its
-// own format).
-__device__ __forceinline__ void load_batch(FfnBatch &b, const FfnBatch *src) {
-  b = *src;
-  for (int j = 0; j < b.n; ++j)
-    if (b.e[j].bits == 0) b.e[j].bits = reinterpret_cast<const ExpertHeader *>(b.e[j].buf)->bits;
 }
 
 struct Ring {
   uint64_t full[kMaxStages], empty[kMaxStages];
 };
 
-__device__ __forceinline__ void ring_init(Ring &r, int stages) {
-  for (int s = 0; s < stages; ++s) {
-    mbar_init(&r.full[s], 1);
-    mbar_init(&r.empty[s], kConsumers);
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
 // ----------------------------------------------------------------- tiles
-// Phase A tile = rows [r0, r0+R) of W1_j and W3_j of one expert; smem layout
-// [W1 codes R*rb][W3 codes R*rb][W1 sz R*szb][W3 sz R*szb].
-// Phase B tile = rows [r0, r0+RB) of W2 of every expert; per expert j
-// [codes RB*rb_j][sz RB*szb_j].
+// Phase A tile = rows [r0, r0+nr) of W1_j and W3_j of one expert (contiguous
+// in the buffer); smem [W1 codes R*rb][W3 codes R*rb][W1 sz R*szb][W3 sz R*szb]
+// with R = rows_pt[j].  Phase B tile = columns [k0, k0+nc) of nr (<= 16)
+// consecutive rows of W2_j; smem [codes nr * nc*b/8][sz nr * nc/8] (one bulk
+// copy per row and region).  The producer publishes each stage's tile in
+// meta[stage] before arming its barrier, so consumers never search or divide.
 
 __device__ __forceinline__ int up_rows_per_tile(int64_t rb, int64_t szb) {
   int R = (int)(kStageBytes / (2 * (rb + szb)));
@@ -243,49 +195,80 @@ __device__ __forceinline__ int up_rows_per_tile(int64_t rb, int64_t szb) {
 }
 
 struct Plan {
-  int n_a;                                  // phase A tiles
+  int n_a;                                  // phase A tiles (grabbed dynamically)
   int RBB, n_blk;                           // phase B: rows per CTA row block, number of row blocks
   int tile_off[kMaxFfnExperts + 1], rows_pt[kMaxFfnExperts];
   int lay_off[kMaxFfnExperts + 1];          // activation layout offsets (floats)
-  int rows_b[kMaxFfnExperts];               // phase B rows per tile, per expert
-  int tiles_b[kMaxFfnExperts + 1];          // phase B tiles per row block, prefix over experts
+  int colsB[kMaxFfnExperts], ktiles[kMaxFfnExperts];  // phase B: W2 columns per tile, tiles per row set
 };
 
-__device__ void make_plan(const FfnBatch &b, Plan &p, int grid) {
+struct TileMeta {
+  int j;      // expert; -1 = end of phase A, -2 = end of phase B
+  int r0;     // phase A: first row of W1/W3; phase B: first output row
+  int nr;     // rows in the tile
+  int k0;     // phase B: first column of W2
+  int nc;     // phase B: columns
+  int flush;  // phase B: last tile of its row sub-block
+  int pad[2];
+};
+
+// Warp 0 builds the plan: lane j fills expert j, offsets by shuffle scans.
+__device__ __forceinline__ void make_plan_warp(const FfnBatch &b, Plan &p, int grid, int lane) {
   const int H = b.H;
-  int t = 0, off = 0, tb = 0;
-  // phase B row block: ~H / grid rows so every CTA owns one block
-  int RBB = (H + grid - 1) / grid;
-  RBB = RBB < 1 ? 1 : RBB;
-  p.RBB = RBB;
-  p.n_blk = (H + RBB - 1) / RBB;
-  for (int j = 0; j < b.n; ++j) {
-    const int bits = b.e[j].bits, I = b.e[j].I;
-    const int R = up_rows_per_tile((int64_t)H * bits / 8, sz_row_bytes(H, bits));
-    p.rows_pt[j] = R;
-    p.tile_off[j] = t;
-    t += (I + R - 1) / R;
-    p.lay_off[j] = off;
-    off += (I + I / slot_cols(bits_slot(bits)) + 3) / 4 * 4;
-    const int64_t rowb = (int64_t)I * bits / 8 + sz_row_bytes(I, bits);
-    int rb = (int)(kStageBytes / rowb);
-    rb = rb < 1 ? 1 : (rb > RBB ? RBB : rb);
-    p.rows_b[j] = rb;
-    p.tiles_b[j] = tb;
-    tb += (RBB + rb - 1) / rb;
+  int tiles = 0, I = 0, R = 1, colsB = 1, kt = 0;
+  if (lane < b.n) {
+    const int bits = b.e[lane].bits;
+    I = b.e[lane].I;
+    R = up_rows_per_tile((int64_t)H * bits / 8, sz_row_bytes(H, bits));
+    tiles = (I + R - 1) / R;
+    // W2 columns per tile: kSubRows rows must fit one stage and a row's 16-byte
+    // chunks must fit 3 chunk groups of 32 lanes (kMaxBChunks)
+    const int per128 = 16 * bits + (bits == 16 ? 0 : 16);  // bytes per 128 columns of one row
+    int cols = kStageBytes / (kSubRows * per128) * 128;
+    const int by_chunks = kMaxBChunks * (bits == 16 ? 8 : 128 / bits);
+    cols = cols < by_chunks ? cols : by_chunks;
+    colsB = cols < I ? cols : I;
+    kt = (I + colsB - 1) / colsB;
   }
-  p.tile_off[b.n] = t;
-  p.lay_off[b.n] = off;
-  p.tiles_b[b.n] = tb;
-  p.n_a = t;
+  int ts = tiles, is = I;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, ts, o), c = __shfl_up_sync(0xffffffffu, is, o);
+    if (lane >= o) ts += a, is += c;
+  }
+  if (lane < b.n) {
+    p.tile_off[lane] = ts - tiles;
+    p.rows_pt[lane] = R;
+    p.lay_off[lane] = is - I;
+    p.colsB[lane] = colsB;
+    p.ktiles[lane] = kt;
+  }
+  if (lane == b.n - 1) {
+    p.tile_off[b.n] = ts;
+    p.lay_off[b.n] = is;
+    p.n_a = ts;
+  }
+  if (lane == 0) {
+    int RBB = (H + grid - 1) / grid;
+    RBB = RBB < 1 ? 1 : RBB;
+    p.RBB = RBB;
+    p.n_blk = (H + RBB - 1) / RBB;
+  }
 }
 
 __device__ unsigned int g_grid_barrier = 0;
 
 // per-CTA phase timestamps of the last launch (globaltimer ns), diagnostics only
 __device__ unsigned long long g_k3_prof[160][8];
-// CTA 0 per-tile timeline of the last launch: [tile][issue, full seen by warp 1, released by warp 1]
-__device__ unsigned long long g_k3_tiles[64][3];
+// CTA 0 per-warp tile timeline of the last launch (clock64 cycles):
+//   producer (warp 0): [tile][empty-wait start, empty passed, copies issued]
+//   consumer warp w:   [tile][full-wait start, full passed, stage released]
+constexpr int kTraceTiles = 48;
+__device__ long long g_k3_trace[17][kTraceTiles][3];
+// CTA 0, consumer warp 1, first 8 phase-A rows: [row][after dots, after warp sums, after store]
+__device__ long long g_k3_sub[8][4];
+#define K3_TRACE(w, t, slot) \
+  do { if (blockIdx.x == 0 && lane == 0 && (t) < kTraceTiles) g_k3_trace[w][t][slot] = clock64(); } while (0)
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -299,9 +282,10 @@ __device__ __forceinline__ void grid_barrier() {
   __threadfence();
   const unsigned int old = atomicAdd(&g_grid_barrier, 1u);
   const unsigned int target = (old / gridDim.x + 1u) * gridDim.x;
-  while ((int)(*(volatile unsigned int *)&g_grid_barrier - target) < 0) {
-  }
-  __threadfence();
+  unsigned int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&g_grid_barrier) : "memory");
+  } while ((int)(v - target) < 0);
 }
 
 // x laid out for every width: slot s (chunk width cols = 8, 16, 32, 64
@@ -312,46 +296,185 @@ __global__ void build_xlay_kernel(const float *__restrict__ x, int H, float4 *__
   extern __shared__ float xs_raw[];
   for (int i = threadIdx.x; i < H; i += blockDim.x) xs_raw[i] = x[i];
   __syncthreads();
-  const int stride = H / 4 + H / 32;
-  for (int sl = 0; sl < 4; ++sl) {
-    const int cols = 8 << sl, nch = H / cols, nq = cols / 4;
-    float4 *xt = xlay + sl * stride;
-    float *sums = reinterpret_cast<float *>(xt + H / 4);
-    for (int i = threadIdx.x; i < H / 4; i += blockDim.x) {
-      const int c = (4 * i) / cols, m = ((4 * i) % cols) / 4;
-      xt[m * nch + c] = reinterpret_cast<const float4 *>(xs_raw)[i];
-    }
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
-      float acc = 0.f;
-      for (int m = 0; m < nq; ++m) {
-        const float4 q = reinterpret_cast<const float4 *>(xs_raw)[(c * cols) / 4 + m];
-        acc += (q.x + q.y) + (q.z + q.w);
+  write_xlay(xs_raw, H, xlay, threadIdx.x, blockDim.x);
+}
+
+// Phase A: this lane's partial dots of row `row` of W1 and W3 in a tile.
+// HT = compile-time hidden size (0: runtime H), so the chunk loop is fully
+// unrolled and every shared-memory offset is an immediate.
+template <int BITS, int HT>
+__device__ __forceinline__ void up_pair(const uint8_t *__restrict__ tile, int R, int row, int H_rt,
+                                        const float4 *__restrict__ xt, const float *__restrict__ xs, int lane,
+                                        float &u, float &v) {
+  const int H = HT ? HT : H_rt;
+  const int rb = H * BITS / 8;
+  const int nch = rb / 16;  // 16-byte chunks per row = stride of the x layout for this width
+  const uint4 *q1 = reinterpret_cast<const uint4 *>(tile + row * rb);
+  const uint4 *q3 = reinterpret_cast<const uint4 *>(tile + (R + row) * rb);
+  const int iters = (nch + 31) / 32;
+  if constexpr (BITS == 16) {
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+    constexpr int kU = 2;
+#pragma unroll kU
+    for (int i = 0; i < iters; ++i) {
+      const int c = lane + 32 * i;
+      if ((HT && (HT * BITS / 8 / 16) % 32 == 0) || c < nch) {
+        const uint4 w1 = q1[c], w3 = q3[c];
+        const float4 x0 = xt[c], x1 = xt[nch + c];
+        a0 = bf_dot(w1.x, lo2(x0), a0);
+        a1 = bf_dot(w1.y, hi2(x0), a1);
+        b0 = bf_dot(w3.x, lo2(x0), b0);
+        b1 = bf_dot(w3.y, hi2(x0), b1);
+        a0 = bf_dot(w1.z, lo2(x1), a0);
+        a1 = bf_dot(w1.w, hi2(x1), a1);
+        b0 = bf_dot(w3.z, lo2(x1), b0);
+        b1 = bf_dot(w3.w, hi2(x1), b1);
       }
-      sums[c] = acc;
+    }
+    u = (a0.x + a0.y) + (a1.x + a1.y);
+    v = (b0.x + b0.y) + (b1.x + b1.y);
+  } else {
+    constexpr int qpw = 32 / BITS / 4;               // activation quads per 32-bit code word
+    constexpr int cpg = kGroup / (128 / BITS);       // chunks per quantization group
+    const int szb = H / 8;                           // (scale, zero) bytes per row
+    const float2 *z1 = reinterpret_cast<const float2 *>(tile + 2 * R * rb + row * szb);
+    const float2 *z3 = reinterpret_cast<const float2 *>(tile + 2 * R * rb + (R + row) * szb);
+    float s1 = 0.f, s3 = 0.f;
+    constexpr int kUq = 1;
+#pragma unroll kUq
+    for (int i = 0; i < iters; ++i) {
+      const int c = lane + 32 * i;
+      if ((HT && (HT * BITS / 8 / 16) % 32 == 0) || c < nch) {
+        const uint4 w1 = q1[c], w3 = q3[c];
+        float2 p0 = make_float2(0.f, 0.f), p1 = p0, r0 = p0, r1 = p0;
+        float4 xv[4];
+#define FATE_WORD(WI)                                                                          \
+  _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) xv[qi] = xt[((WI) * qpw + qi) * nch + c]; \
+  word_dot<BITS>(word<WI>(w1), xv, p0, p1);                                                    \
+  word_dot<BITS>(word<WI>(w3), xv, r0, r1);
+        FATE_WORD(0) FATE_WORD(1) FATE_WORD(2) FATE_WORD(3)
+#undef FATE_WORD
+        const float xsum = xs[c];
+        const float2 g1 = z1[c / cpg], g3 = z3[c / cpg];
+        s1 = fmaf(g1.x, (p0.x + p0.y) + (p1.x + p1.y), fmaf(g1.y, xsum, s1));
+        s3 = fmaf(g3.x, (r0.x + r0.y) + (r1.x + r1.y), fmaf(g3.y, xsum, s3));
+      }
+    }
+    u = s1;
+    v = s3;
+  }
+}
+
+// Phase B: chunk c of a tile (global chunk cg of expert j's activation layout
+// `at`, nchI chunks per activation quad row) for MR rows of the tile,
+// row[i] = 4 m_i + w4, valid[i] = row exists; out[i] = w_j * dot(row[i]).
+template <int BITS, int MR>
+__device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, int c, const float4 *__restrict__ at,
+                                           int nchI, int cg, const int (&row)[MR], int valid, float wj,
+                                           float (&out)[MR]) {
+  const int rowb = nc * BITS / 8;
+  uint4 q[MR];
+#pragma unroll
+  for (int i = 0; i < MR; ++i)
+    q[i] = (valid >> i & 1) ? reinterpret_cast<const uint4 *>(tile + row[i] * rowb)[c] : make_uint4(0, 0, 0, 0);
+  float2 p[MR][2];
+#pragma unroll
+  for (int i = 0; i < MR; ++i) p[i][0] = p[i][1] = make_float2(0.f, 0.f);
+  if constexpr (BITS == 16) {
+    const float4 x0 = at[cg], x1 = at[nchI + cg];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      p[i][0] = bf_dot(q[i].x, lo2(x0), p[i][0]);
+      p[i][1] = bf_dot(q[i].y, hi2(x0), p[i][1]);
+      p[i][0] = bf_dot(q[i].z, lo2(x1), p[i][0]);
+      p[i][1] = bf_dot(q[i].w, hi2(x1), p[i][1]);
+    }
+#pragma unroll
+    for (int i = 0; i < MR; ++i) out[i] = wj * ((p[i][0].x + p[i][0].y) + (p[i][1].x + p[i][1].y));
+  } else {
+    constexpr int qpw = 32 / BITS / 4;
+    float2 sa = make_float2(0.f, 0.f);
+    float4 xv[4];
+#define FATE_WORD(WI)                                                   \
+  _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                  \
+    xv[qi] = at[((WI) * qpw + qi) * nchI + cg];                         \
+    sa = fadd2(sa, fadd2(lo2(xv[qi]), hi2(xv[qi])));                    \
+  }                                                                     \
+  _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]);
+    FATE_WORD(0) FATE_WORD(1) FATE_WORD(2) FATE_WORD(3)
+#undef FATE_WORD
+    const float xsum = sa.x + sa.y;
+    const int szr = nc / 8;  // bytes of (scale, zero) pairs per row
+    const int grp = c / (kGroup / (128 / BITS));
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const float2 z = (valid >> i & 1) ? reinterpret_cast<const float2 *>(tile + nr * rowb + row[i] * szr)[grp]
+                                        : make_float2(0.f, 0.f);
+      const float s = (p[i][0].x + p[i][0].y) + (p[i][1].x + p[i][1].y);
+      out[i] = wj * fmaf(z.x, s, z.y * xsum);
     }
   }
 }
 
+// Rows of a phase B tile owned by consumer warp cw (12 warps): with 3 chunk
+// groups (G = 3) warp cw takes chunk group cw / 4 and rows r = 4m + cw % 4
+// (m = 0..3); with one group (G = 1, at most 32 chunks per row) it takes rows
+// cw and cw + 12.  Either way r = 4m + (cw & 3), so every thread's rows stay in
+// acc[m] for the whole sub-block whatever the tile's chunk-group count.
+template <int BITS, int MR>
+__device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, int c, const float4 *__restrict__ at,
+                                          int nchI, int cg, int cw, float wj, float (&acc)[4]) {
+  int m[MR], row[MR], valid = 0;
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    m[i] = MR == 4 ? i : (cw >> 2) + 3 * i;
+    row[i] = 4 * m[i] + (cw & 3);
+    if (row[i] < nr) valid |= 1 << i;
+  }
+  float out[MR];
+  down_chunk<BITS, MR>(tile, nr, nc, c, at, nchI, cg, row, valid, wj, out);
+#pragma unroll
+  for (int i = 0; i < MR; ++i) {
+    if constexpr (MR == 4) {
+      acc[i] += out[i];
+    } else {
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) acc[mm] += (m[i] == mm && (valid >> i & 1)) ? out[i] : 0.f;
+    }
+  }
+}
+
+// One phase B tile: the 12 consumer warps split the tile's chunks into G
+// groups of 32 lanes (G = 1 or 3) and its rows into 12 / G residue classes.
 template <int BITS>
-__device__ __forceinline__ void up_pair_dots(const uint8_t *c1, const uint8_t *c3, const float2 *z1, const float2 *z3,
-                                             const float4 *xt, const float *xs, int nch, int lane, float &u, float &v) {
-  const uint8_t *const cs[2] = {c1, c3};
-  const float2 *const zs[2] = {z1, z3};
-  float out[2];
-  rows_dot_smem<BITS, 2>(cs, zs, xt, xs, nch, lane, 32, out);
-  u = out[0];
-  v = out[1];
+__device__ __forceinline__ void down_tile_bits(const TileMeta &tm, const uint8_t *tile, const FfnExpert &ex,
+                                               const float *al_j, int cw, int lane, float (&acc)[4]) {
+  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;  // columns per 16-byte chunk
+  const int nch = tm.nc / cols;
+  const bool g3 = nch > 32;
+  const int c = lane + (g3 ? 32 * (cw >> 2) : 0);
+  if (c >= nch) return;
+  const float4 *at = reinterpret_cast<const float4 *>(al_j);
+  const int nchI = ex.I / cols, cg = tm.k0 / cols + c;
+  if (g3) down_tile<BITS, 4>(tile, tm.nr, tm.nc, c, at, nchI, cg, cw, ex.weight, acc);
+  else down_tile<BITS, 2>(tile, tm.nr, tm.nc, c, at, nchI, cg, cw, ex.weight, acc);
 }
 
 // One launch per decode step:
-//   phase A  gate+up rows: a = silu(W1 x) * (W3 x), written straight into the
-//            chunk-transposed activation layout of its expert (alay, global);
+//   phase A  gate+up rows: a = silu(W1 x) * (W3 x).  Tiles go round-robin
+//            over the CTAs; warp w takes the rows of tile k whose running index
+//            is w mod 16, so the rows of consecutive tiles land on different
+//            warps; a goes straight into the chunk-transposed layout of its
+//            expert (alay, global);
 //   barrier  grid-wide (all CTAs resident) so every activation is visible;
-//   phase B  each CTA owns a block of output rows and streams those rows of W2
-//            of every expert, per-expert tiles; partials are combined in a
-//            fixed order, so y is deterministic.
+//   phase B  each CTA owns a block of output rows (sub-blocks of <= 16) and
+//            streams column ranges of those rows of W2 of every expert; the
+//            16 consumer warps split the columns (chunk groups) and rows
+//            (r = 4m + w%4), accumulating w_j * dot in registers across all
+//            tiles, then one fixed-order reduction per row: y is deterministic.
 // The producer never waits for the barrier: W2 tiles are in flight while
 // phase A drains.
+template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
                                                           const float4 *__restrict__ xlay, float *__restrict__ alay,
                                                           float *__restrict__ y, unsigned long long *bytes_stat,
@@ -360,147 +483,210 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
   __shared__ FfnBatch batch;
   __shared__ Plan plan;
   __shared__ Ring ring;
-  __shared__ __align__(8) uint64_t aux_bar[2];
-  __shared__ float red[kMaxStages][kConsumers];
-  __shared__ int cnt[kMaxStages][kConsumers];
+  __shared__ TileMeta meta[kMaxStages];
+  __shared__ __align__(8) uint64_t x_bar, act_bar[kMaxFfnExperts];
+  __shared__ float part[kSubRows][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned long long *prof = g_k3_prof[blockIdx.x < 160 ? blockIdx.x : 159];
-  if (tid < 32) {
-    // warp 0: batch copy with 16-byte loads, then the plan (lane 0)
+  if (blockIdx.x == 0)
+    for (int i = tid; i < 17 * kTraceTiles * 3; i += kThreads) (&g_k3_trace[0][0][0])[i] = 0;
+  if (warp == 0) {
+    // warp 0: batch copy with 16-byte loads, the plan, the barriers
     const int4 *src = reinterpret_cast<const int4 *>(batch_p);
     int4 *dst = reinterpret_cast<int4 *>(&batch);
-    for (int i = tid; i < (int)(sizeof(FfnBatch) / 16); i += 32) dst[i] = __ldg(src + i);
+    for (int i = lane; i < (int)(sizeof(FfnBatch) / 16); i += 32) dst[i] = __ldg(src + i);
     __syncwarp();
-    if (tid == 0) {
+    if (lane < batch.n && batch.e[lane].bits == 0)
+      batch.e[lane].bits = reinterpret_cast<const ExpertHeader *>(batch.e[lane].buf)->bits;
+    __syncwarp();
+    make_plan_warp(batch, plan, gridDim.x, lane);
+    if (lane == 0) {
       prof[0] = gtime();
-      for (int j = 0; j < batch.n; ++j)
-        if (batch.e[j].bits == 0) batch.e[j].bits = reinterpret_cast<const ExpertHeader *>(batch.e[j].buf)->bits;
-      make_plan(batch, plan, gridDim.x);
-      if (bytes_stat && blockIdx.x == 0) {
-        unsigned long long bytes = 0;
-        for (int j = 0; j < batch.n; ++j) bytes += make_layout(batch.H, batch.e[j].I, batch.e[j].bits).payload;
-        atomicAdd(bytes_stat, bytes);
+      for (int s = 0; s < stages; ++s) {
+        mbar_init(&ring.full[s], 1);
+        mbar_init(&ring.empty[s], kConsumers);
       }
-      ring_init(ring, stages);
-      mbar_init(&aux_bar[0], 1);
-      mbar_init(&aux_bar[1], 1);
+      mbar_init(&x_bar, 1);
+      for (int j = 0; j < batch.n; ++j) mbar_init(&act_bar[j], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
-  for (int q = tid; q < kMaxStages * kConsumers; q += kThreads) (&cnt[0][0])[q] = 0;
   __syncthreads();
-  const int H = batch.H;
+  const int H = HT ? HT : batch.H;
   const int lay_stride = H / 4 + H / 32;
   uint8_t *ring_buf = smem;
   float4 *xl = reinterpret_cast<float4 *>(smem + (size_t)stages * kStageBytes);  // x layouts (phase A)
   float *al = reinterpret_cast<float *>(xl);                                      // activation layouts (phase B)
-  float *psum = reinterpret_cast<float *>(smem + (size_t)stages * kStageBytes) + plan.lay_off[batch.n] +
-                plan.lay_off[batch.n] / 8 + 64;  // [n][RBB] weighted partials (after the activation region)
   if (warp == 0) {
-    // ================= producer (one elected lane)
+    // ================= producer warp: lane 0 arms stages, lanes issue copies
     if (lane == 0) {
       const uint32_t xbytes = (uint32_t)(4 * lay_stride * 16);
-      mbar_expect_tx(&aux_bar[0], xbytes);
-      bulk_g2s(xl, xlay, xbytes, &aux_bar[0]);
-      int stage = 0, ti = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < plan.n_a; t += gridDim.x) {
+      mbar_expect_tx(&x_bar, xbytes);
+      bulk_g2s(xl, xlay, xbytes, &x_bar);
+      if (blockIdx.x == 0 && bytes_stat) {
+        unsigned long long bytes = 0;
+        for (int j = 0; j < batch.n; ++j) bytes += make_layout(H, batch.e[j].I, batch.e[j].bits).payload;
+        atomicAdd(bytes_stat, bytes);
+      }
+    }
+    int stage = 0, ti = 0;
+    uint32_t phase = 0;
+    // one phase A tile (or the end marker); returns true at the end
+    auto step_a = [&](int t) -> bool {
+      K3_TRACE(0, ti, 0);
+      mbar_wait(&ring.empty[stage], phase ^ 1);
+      K3_TRACE(0, ti, 1);
+      const bool end = t >= plan.n_a;
+      if (end) {
+        if (lane == 0) {
+          meta[stage].j = -1;
+          mbar_arrive(&ring.full[stage]);
+        }
+      } else {
         int j = 0;
         while (t >= plan.tile_off[j + 1]) ++j;
         const FfnExpert &ex = batch.e[j];
-        const Layout L = make_layout(H, ex.I, ex.bits);
-        if (blockIdx.x == 0 && ti < 64) g_k3_tiles[ti][0] = 0;
+        const int bits = ex.bits;
         const int R = plan.rows_pt[j];
         const int r0 = (t - plan.tile_off[j]) * R, nr = min(R, ex.I - r0);
-        const int64_t rb = L.row_bytes_up, szb = sz_row_bytes(H, ex.bits);
-        const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
-        mbar_wait(&ring.empty[stage], phase ^ 1);
-        if (blockIdx.x == 0 && ti < 64) g_k3_tiles[ti][0] = gtime();
-        ++ti;
+        const uint32_t rb = (uint32_t)H * bits / 8, szb = bits == 16 ? 0u : (uint32_t)H / 8;
+        const uint32_t cb = nr * rb, sb = nr * szb;
         uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
-        const uint32_t cb = (uint32_t)(nr * rb), sb = (uint32_t)(nr * szb);
-        mbar_expect_tx(&ring.full[stage], 2 * (cb + sb));
-        bulk_g2s(dst, p + L.c1 + r0 * rb, cb, &ring.full[stage]);
-        bulk_g2s(dst + R * rb, p + L.c3 + r0 * rb, cb, &ring.full[stage]);
-        if (sb) {
-          bulk_g2s(dst + 2 * R * rb, p + L.s1 + r0 * szb, sb, &ring.full[stage]);
-          bulk_g2s(dst + 2 * R * rb + R * szb, p + L.s3 + r0 * szb, sb, &ring.full[stage]);
+        if (lane == 0) {
+          meta[stage].j = j;
+          meta[stage].r0 = r0;
+          meta[stage].nr = nr;
+          mbar_expect_tx(&ring.full[stage], 2 * (cb + sb));
         }
-        if (++stage == stages) stage = 0, phase ^= 1;
+        __syncwarp();
+        if (lane < (sb ? 4 : 2)) {
+          // lanes 0..3: W1 codes, W3 codes, W1 (scale, zero), W3 (scale, zero)
+          const int64_t n = (int64_t)H * ex.I, cbytes = bits == 16 ? 2 * n : n * bits / 8;
+          const int64_t sbytes = n / kGroup * 8;
+          const int64_t src = lane == 0 ? (int64_t)r0 * rb
+                            : lane == 1 ? cbytes + (int64_t)r0 * rb
+                            : lane == 2 ? 3 * cbytes + (int64_t)r0 * szb
+                                        : 3 * cbytes + sbytes + (int64_t)r0 * szb;
+          const uint32_t off = lane == 0 ? 0u : lane == 1 ? R * rb : lane == 2 ? 2 * R * rb : 2 * R * rb + R * szb;
+          bulk_g2s(dst + off, ex.buf + FATE_HEADER_BYTES + src, lane < 2 ? cb : sb, &ring.full[stage]);
+        }
       }
-      for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x) {
-        const int R0 = blk * plan.RBB, nrb = min(plan.RBB, H - R0);
+      K3_TRACE(0, ti, 2);
+      ++ti;
+      if (++stage == stages) stage = 0, phase ^= 1;
+      return end;
+    };
+    // static round-robin over the tile list (expert-major, so every CTA gets
+    // a proportional mix of each expert's format); then the end marker
+    for (int t = blockIdx.x;; t += gridDim.x)
+      if (step_a(t)) break;
+    for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x) {
+      const int R0 = blk * plan.RBB, rows = min(plan.RBB, H - R0);
+      for (int s0 = 0; s0 < rows; s0 += kSubRows) {
+        const int nr = min(kSubRows, rows - s0), rs0 = R0 + s0;
         for (int j = 0; j < batch.n; ++j) {
           const FfnExpert &ex = batch.e[j];
-          const Layout L = make_layout(H, ex.I, ex.bits);
-          const int64_t rb = L.row_bytes_down, szb = sz_row_bytes(ex.I, ex.bits);
+          const int bits = ex.bits;
+          const Layout L = make_layout(H, ex.I, bits);
+          const int64_t rb = L.row_bytes_down, szb = sz_row_bytes(ex.I, bits);
           const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
-          const int rt = plan.rows_b[j];
-          for (int q0 = 0; q0 < nrb; q0 += rt) {
-            const int nr = min(rt, nrb - q0), r0 = R0 + q0;
+          for (int kt = 0; kt < plan.ktiles[j]; ++kt) {
+            const int k0 = kt * plan.colsB[j], nc = min(plan.colsB[j], ex.I - k0);
+            const uint32_t cb = (uint32_t)nc * bits / 8, sb = bits == 16 ? 0u : (uint32_t)nc / 8;
+            K3_TRACE(0, ti, 0);
             mbar_wait(&ring.empty[stage], phase ^ 1);
-            if (blockIdx.x == 0 && ti < 64) g_k3_tiles[ti][0] = gtime();
-            ++ti;
+            K3_TRACE(0, ti, 1);
             uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
-            mbar_expect_tx(&ring.full[stage], (uint32_t)(nr * (rb + szb)));
-            bulk_g2s(dst, p + L.c2 + r0 * rb, (uint32_t)(nr * rb), &ring.full[stage]);
-            if (szb) bulk_g2s(dst + rt * rb, p + L.s2 + r0 * szb, (uint32_t)(nr * szb), &ring.full[stage]);
+            if (lane == 0) {
+              TileMeta &m = meta[stage];
+              m.j = j;
+              m.r0 = rs0;
+              m.nr = nr;
+              m.k0 = k0;
+              m.nc = nc;
+              m.flush = (j == batch.n - 1 && kt == plan.ktiles[j] - 1);
+              mbar_expect_tx(&ring.full[stage], (uint32_t)nr * (cb + sb));
+            }
+            __syncwarp();
+            if (nc == ex.I) {
+              // whole rows: the tile's rows are contiguous in the buffer, one copy
+              // for the codes and one for the (scale, zero) pairs
+              if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)rs0 * rb, nr * cb, &ring.full[stage]);
+              if (lane == 1 && sb) bulk_g2s(dst + nr * cb, p + L.s2 + (int64_t)rs0 * szb, nr * sb, &ring.full[stage]);
+            } else if (lane < nr) {
+              const int64_t r = rs0 + lane;
+              bulk_g2s(dst + lane * cb, p + L.c2 + r * rb + (int64_t)k0 * bits / 8, cb, &ring.full[stage]);
+              if (sb) bulk_g2s(dst + nr * cb + lane * sb, p + L.s2 + r * szb + k0 / 8, sb, &ring.full[stage]);
+            }
+            K3_TRACE(0, ti, 2);
+            ++ti;
             if (++stage == stages) stage = 0, phase ^= 1;
           }
         }
       }
-      prof[7] = gtime();
     }
+    if (lane == 0) prof[7] = gtime();
     return;
   }
   // ================= consumers
-  const int ctid = tid - 32, cthr = 32 * kConsumers, cw = warp - 1;
+  const int ctid = tid - 32, cw = warp - 1;
   if (ctid == 0) prof[1] = gtime();
-  mbar_wait(&aux_bar[0], 0);  // x layouts landed
+  mbar_wait(&x_bar, 0);  // x layouts landed
   if (ctid == 0) prof[2] = gtime();
-  // ---- phase A: each warp walks the ring on its own; in tile t it takes
-  // rows with (row + k) % kConsumers == warp, both W1 and W3 of the row
-  int stage = 0;
+  int stage = 0, k = 0, rot = 0;
   uint32_t phase = 0;
-  int k = 0;
-  for (int t = blockIdx.x; t < plan.n_a; t += gridDim.x, ++k) {
-    int j = 0;
-    while (t >= plan.tile_off[j + 1]) ++j;
+  for (;; ++k) {
+    K3_TRACE(warp, k, 0);
+    mbar_wait(&ring.full[stage], phase);
+    K3_TRACE(warp, k, 1);
+    const int j = meta[stage].j;
+    if (j < 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[stage]);
+      if (++stage == stages) stage = 0, phase ^= 1;
+      ++k;
+      break;
+    }
+    const int r0 = meta[stage].r0, nr = meta[stage].nr;
     const FfnExpert &ex = batch.e[j];
-    const int bits = ex.bits, sl = bits_slot(bits), cols = slot_cols(sl);
+    const int bits = ex.bits, sl = bits_slot(bits);
     const int R = plan.rows_pt[j];
-    const int r0 = (t - plan.tile_off[j]) * R, nr = min(R, ex.I - r0);
-    const int64_t rb = (int64_t)H * bits / 8, szb = sz_row_bytes(H, bits);
-    const int nch = (int)(rb / 16);
     const float4 *xt = xl + sl * lay_stride;
     const float *xs = reinterpret_cast<const float *>(xl + sl * lay_stride + H / 4);
-    float *aj = alay + plan.lay_off[j];
-    const int nch_a = ex.I / cols;
-    mbar_wait(&ring.full[stage], phase);
-    if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 64) g_k3_tiles[k][1] = gtime();
     const uint8_t *tile = ring_buf + (size_t)stage * kStageBytes;
-    for (int row = (cw - k % kConsumers + kConsumers) % kConsumers; row < nr; row += kConsumers) {
-      const uint8_t *c1 = tile + row * rb, *c3 = tile + (R + row) * rb;
-      const float2 *z1 = reinterpret_cast<const float2 *>(tile + 2 * R * rb + row * szb);
-      const float2 *z3 = reinterpret_cast<const float2 *>(tile + 2 * R * rb + (R + row) * szb);
+    // W2 chunk width of this expert (power of two): a[r] -> (r/cols, (r%cols)/4, r&3)
+    const int lc = bits == 16 ? 3 : bits == 8 ? 4 : bits == 4 ? 5 : 6;
+    float *aj = alay + plan.lay_off[j];
+    const int nch_a = ex.I >> lc;
+    int row0 = cw - rot;
+    if (row0 < 0) row0 += kConsumers;
+    for (int row = row0; row < nr; row += kConsumers) {
       float u, v;
       switch (bits) {
-        case 16: up_pair_dots<16>(c1, c3, z1, z3, xt, xs, nch, lane, u, v); break;
-        case 8: up_pair_dots<8>(c1, c3, z1, z3, xt, xs, nch, lane, u, v); break;
-        case 4: up_pair_dots<4>(c1, c3, z1, z3, xt, xs, nch, lane, u, v); break;
-        default: up_pair_dots<2>(c1, c3, z1, z3, xt, xs, nch, lane, u, v); break;
+        case 16: up_pair<16, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
+        case 8: up_pair<8, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
+        case 4: up_pair<4, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
+        default: up_pair<2, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
       }
+      const long long c0 = clock64();
       u = warp_sum(u);
       v = warp_sum(v);
+      const long long c1 = clock64();
       if (lane == 0) {
         // straight into the chunk-transposed activation layout of phase B
-        const int r = r0 + row, c = r / cols, m = (r % cols) / 4;
+        const int r = r0 + row, c = r >> lc, m = (r & ((1 << lc) - 1)) >> 2;
         aj[(m * nch_a + c) * 4 + (r & 3)] = u / (1.0f + expf(-u)) * v;
       }
+      if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 8) {
+        g_k3_sub[k][0] = c0;
+        g_k3_sub[k][1] = c1;
+        g_k3_sub[k][2] = clock64();
+      }
     }
+    rot = (rot + nr) % kConsumers;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[stage]);
-    if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 64) g_k3_tiles[k][2] = gtime();
+    K3_TRACE(warp, k, 2);
     if (++stage == stages) stage = 0, phase ^= 1;
   }
   // ---- every CTA's activations are complete and visible
@@ -509,91 +695,56 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     prof[3] = gtime();
     grid_barrier();
     prof[4] = gtime();
-    // one bulk copy of every expert's activation layout (chunk sums are local)
-    const uint32_t abytes = (uint32_t)(plan.lay_off[batch.n] * 4);
-    mbar_expect_tx(&aux_bar[1], abytes);
+    // per-expert bulk copies of the activation layouts, in phase-B order
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    bulk_g2s(al, alay, abytes, &aux_bar[1]);
-  }
-  mbar_wait(&aux_bar[1], 0);
-  for (int j = 0; j < batch.n; ++j) {
-    const int I = batch.e[j].I, cols = slot_cols(bits_slot(batch.e[j].bits));
-    const int nch = I / cols, nq = cols / 4;
-    const float4 *xt = reinterpret_cast<const float4 *>(al + plan.lay_off[j]);
-    float *sums = al + plan.lay_off[j] + I;
-    for (int c = ctid; c < nch; c += cthr) {
-      float acc = 0.f;
-      for (int m = 0; m < nq; ++m) {
-        const float4 q = xt[m * nch + c];
-        acc += (q.x + q.y) + (q.z + q.w);
-      }
-      sums[c] = acc;
-    }
-  }
-  consumer_sync();
-  if (ctid == 0) prof[5] = gtime();
-  // ---- phase B: per row block, per expert tiles; task (row, part) with
-  // P = kConsumers / rows parts per row; the last part to finish a row writes
-  // the expert's weighted partial; rows are summed over experts in order.
-  for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x) {
-    const int R0 = blk * plan.RBB, nrb = min(plan.RBB, H - R0);
     for (int j = 0; j < batch.n; ++j) {
-      const FfnExpert &ex = batch.e[j];
-      const int bits = ex.bits;
-      const int64_t rb = (int64_t)ex.I * bits / 8, szb = sz_row_bytes(ex.I, bits);
-      const int nch = (int)(rb / 16);
-      const float4 *at = reinterpret_cast<const float4 *>(al + plan.lay_off[j]);
-      const float *as = al + plan.lay_off[j] + ex.I;
-      const int rt = plan.rows_b[j];
-      for (int q0 = 0; q0 < nrb; q0 += rt) {
-        const int nr = min(rt, nrb - q0);
-        const int P = nr >= kConsumers ? 1 : kConsumers / nr;
-        mbar_wait(&ring.full[stage], phase);
-        if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 64) g_k3_tiles[k][1] = gtime();
-        const uint8_t *tile = ring_buf + (size_t)stage * kStageBytes;
-        for (int task = cw; task < (nr >= kConsumers ? nr : nr * P); task += kConsumers) {
-          const int row = nr >= kConsumers ? task : task / P, part = nr >= kConsumers ? 0 : task % P;
-          const uint8_t *codes = tile + row * rb;
-          const float2 *sz = reinterpret_cast<const float2 *>(tile + rt * rb + row * szb);
-          float pj;
-          switch (bits) {
-            case 16: pj = row_dot_smem<16>(codes, sz, at, as, nch, lane + 32 * part, 32 * P); break;
-            case 8: pj = row_dot_smem<8>(codes, sz, at, as, nch, lane + 32 * part, 32 * P); break;
-            case 4: pj = row_dot_smem<4>(codes, sz, at, as, nch, lane + 32 * part, 32 * P); break;
-            default: pj = row_dot_smem<2>(codes, sz, at, as, nch, lane + 32 * part, 32 * P); break;
-          }
-          pj = warp_sum(pj);
-          if (lane == 0) {
-            float *ps = psum + j * plan.RBB + q0 + row;
-            if (P == 1) {
-              *ps = ex.weight * pj;
-            } else {
-              red[stage][task] = pj;
-              __threadfence_block();
-              if (atomicAdd(&cnt[stage][row], 1) == P - 1) {
-                __threadfence_block();
-                float sum = 0.f;
-                for (int q = 0; q < P; ++q) sum += ((volatile float *)red[stage])[row * P + q];
-                *ps = ex.weight * sum;
-                cnt[stage][row] = 0;
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ring.empty[stage]);
-        if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 64) g_k3_tiles[k][2] = gtime();
-        ++k;
-        if (++stage == stages) stage = 0, phase ^= 1;
+      const uint32_t abytes = (uint32_t)(batch.e[j].I * 4);
+      mbar_expect_tx(&act_bar[j], abytes);
+      bulk_g2s(al + plan.lay_off[j], alay + plan.lay_off[j], abytes, &act_bar[j]);
+    }
+  }
+  // ---- phase B: tiles in producer order; flush = last tile of a row sub-block
+  const int w4 = cw & 3;  // this warp's rows are r = 4m + w4
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  bool first = true;
+  int subs_left = 0;  // row sub-blocks this CTA reduces (one flush each)
+  for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x)
+    subs_left += (min(plan.RBB, H - blk * plan.RBB) + kSubRows - 1) / kSubRows;
+  while (subs_left > 0) {
+    K3_TRACE(warp, k, 0);
+    mbar_wait(&ring.full[stage], phase);
+    K3_TRACE(warp, k, 1);
+    const TileMeta tm = meta[stage];
+    const FfnExpert &ex = batch.e[tm.j];
+    mbar_wait(&act_bar[tm.j], 0);
+    if (first && ctid == 0) prof[5] = gtime();
+    first = false;
+    const uint8_t *tile = ring_buf + (size_t)stage * kStageBytes;
+    const float *al_j = al + plan.lay_off[tm.j];
+    switch (ex.bits) {
+      case 16: down_tile_bits<16>(tm, tile, ex, al_j, cw, lane, acc); break;
+      case 8: down_tile_bits<8>(tm, tile, ex, al_j, cw, lane, acc); break;
+      case 4: down_tile_bits<4>(tm, tile, ex, al_j, cw, lane, acc); break;
+      default: down_tile_bits<2>(tm, tile, ex, al_j, cw, lane, acc); break;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[stage]);
+    K3_TRACE(warp, k, 2);
+    ++k;
+    if (++stage == stages) stage = 0, phase ^= 1;
+    if (tm.flush) {
+      // fixed-order reduction: row r = 4m + w4 collects warps w4, w4 + 4, w4 + 8
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float v = warp_sum(acc[m]);
+        if (lane == 0 && 4 * m + w4 < tm.nr) part[4 * m + w4][cw >> 2] = v;
+        acc[m] = 0.f;
       }
+      consumer_sync();
+      if (ctid < tm.nr) y[tm.r0 + ctid] = (part[ctid][0] + part[ctid][1]) + part[ctid][2];
+      consumer_sync();
+      --subs_left;
     }
-    consumer_sync();
-    for (int r = ctid; r < nrb; r += cthr) {
-      float acc = 0.f;
-      for (int j = 0; j < batch.n; ++j) acc += ((volatile float *)psum)[j * plan.RBB + r];  // fixed order
-      y[R0 + r] = acc;
-    }
-    consumer_sync();
   }
   if (ctid == 0) prof[6] = gtime();
 }
@@ -612,17 +763,17 @@ int num_sms() {
 
 // dynamic smem beyond the ring: max(x layouts of every width, activation
 // layouts of every expert with bf16-size chunk sums + the partial-sum table)
-size_t region_bytes(int H, int max_total_I, int max_experts, int grid) {
-  const size_t xb = (size_t)4 * (H / 4 + H / 32) * 16;
-  const int RBB = (H + grid - 1) / grid;
-  const size_t ab = ((size_t)max_total_I + max_total_I / 8 + 4 * max_experts + max_total_I / 8 + 64 +
-                     (size_t)max_experts * RBB) * 4;
+size_t region_bytes(int H, int max_total_I) {
+  const size_t xb = (size_t)4 * (H / 4 + H / 32) * 16;  // x layouts of the four widths (phase A)
+  const size_t ab = (size_t)max_total_I * 4;             // activation layouts of every expert (phase B)
   return xb > ab ? xb : ab;
 }
 
+constexpr size_t kStaticReserve = 4096;  // static shared memory (batch, plan, barriers, partials)
+
 int stages_for(size_t extra) {
   int s = kMaxStages;
-  while (s > 2 && (size_t)s * kStageBytes + extra + 8192 > (size_t)kSmemLimit) --s;
+  while (s > 2 && (size_t)s * kStageBytes + extra + kStaticReserve > (size_t)kSmemLimit) --s;
   return s;
 }
 
@@ -630,9 +781,11 @@ int stages_for(size_t extra) {
 
 cudaError_t ffn_preload() {
   cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, ffn_kernel);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, build_xlay_kernel);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaError_t e = cudaFuncGetAttributes(&a, build_xlay_kernel);
+  const int dyn = (int)(kSmemLimit - kStaticReserve);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   return e;
 }
 
@@ -659,13 +812,18 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
     configured = true;
   }
   const int sms = num_sms();
-  const size_t extra = region_bytes(H, max_total_I, kMaxFfnExperts, sms);
+  const size_t extra = region_bytes(H, max_total_I);
   const int st = stages_for(extra);
   const size_t smem = (size_t)st * kStageBytes + extra;
-  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  if (smem + kStaticReserve > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
   // the grid barrier needs every CTA resident: one CTA per SM, grid = #SMs
-  ffn_kernel<<<sms, kThreads, smem, s>>>(batch_dev, reinterpret_cast<const float4 *>(xlay), alay, y_dev, bytes_stat,
-                                         st);
+  const float4 *xl = reinterpret_cast<const float4 *>(xlay);
+  if (H == 2048)
+    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
+  else if (H == 4096)
+    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
+  else
+    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
   return cudaGetLastError();
 }
 
@@ -673,7 +831,11 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
 
 // Diagnostics: per-CTA phase timestamps of the last K3 launch, [160][8] ns.
 extern "C" int fate_k3_profile(uint64_t *out_host) {
-  if (cudaMemcpyFromSymbol(out_host + 160 * 8, fate::g_k3_tiles, sizeof(unsigned long long) * 64 * 3) != cudaSuccess)
+  if (cudaMemcpyFromSymbol(out_host + 160 * 8 + 17 * fate::kTraceTiles * 3, fate::g_k3_sub, sizeof(long long) * 32) !=
+      cudaSuccess)
+    return FATE_ECUDA;
+  if (cudaMemcpyFromSymbol(out_host + 160 * 8, fate::g_k3_trace, sizeof(long long) * 17 * fate::kTraceTiles * 3) !=
+      cudaSuccess)
     return FATE_ECUDA;
   if (cudaMemcpyFromSymbol(out_host, fate::g_k3_prof, sizeof(unsigned long long) * 160 * 8) != cudaSuccess) {
     fate::set_error("fate_k3_profile: copy failed");
@@ -685,7 +847,7 @@ extern "C" int fate_k3_profile(uint64_t *out_host) {
 extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *const *bufs, const float *weights,
                                float *scratch_dev, float *y_dev, void *stream) {
   using namespace fate;
-  if (n < 1 || n > kMaxFfnExperts || H < 64 || H % 64) {
+  if (n < 1 || n > kMaxFfnExperts || H < 128 || H % 128) {
     set_error("fate_ffn_decode: bad arguments");
     return FATE_EINVAL;
   }
@@ -698,7 +860,7 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
     ExpertHeader h;
     FATE_CUDA(cudaMemcpyAsync(&h, bufs[j], sizeof(h), cudaMemcpyDeviceToHost, s));
     FATE_CUDA(cudaStreamSynchronize(s));
-    if (h.magic != kMagic || h.H != H || h.I % 64) {
+    if (h.magic != kMagic || h.H != H || h.I < 128 || h.I % 128) {
       set_error("fate_ffn_decode: buffer header does not describe a packed expert of this hidden size");
       return FATE_EINVAL;
     }
@@ -720,5 +882,63 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
   FATE_CUDA(e);
   (void)scratch_dev;
   FATE_CUDA(cudaStreamSynchronize(s));  // b lives on this stack frame
+  return FATE_OK;
+}
+
+extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets, const uint8_t *const *bufs,
+                                     const float *weights, float *y_dev, int iters, void *stream, float *ms_out) {
+  using namespace fate;
+  if (n < 1 || n > kMaxFfnExperts || nsets < 1 || nsets > 64 || H < 128 || H % 128 || iters < 1 || !ms_out) {
+    set_error("fate_ffn_decode_timed: bad arguments");
+    return FATE_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<FfnBatch> bs(nsets);
+  int max_off = 0;
+  for (int q = 0; q < nsets; ++q) {
+    FfnBatch &b = bs[q];
+    b = FfnBatch{};
+    b.n = n;
+    b.H = H;
+    int off = 0;
+    for (int j = 0; j < n; ++j) {
+      const uint8_t *buf = bufs[q * n + j];
+      ExpertHeader h;
+      FATE_CUDA(cudaMemcpy(&h, buf, sizeof(h), cudaMemcpyDeviceToHost));
+      if (h.magic != kMagic || h.H != H || h.I < 128 || h.I % 128) {
+        set_error("fate_ffn_decode_timed: buffer header does not describe a packed expert of this hidden size");
+        return FATE_EINVAL;
+      }
+      b.e[j] = FfnExpert{buf, weights[j], h.I, h.bits, off};
+      off += h.I;
+    }
+    b.total_I = off;
+    max_off = off > max_off ? off : max_off;
+  }
+  FfnBatch *bd = nullptr;
+  float *xl = nullptr, *al = nullptr;
+  FATE_CUDA(cudaMalloc(&bd, sizeof(FfnBatch) * nsets));
+  FATE_CUDA(cudaMalloc(&xl, ffn_xlay_floats(H) * sizeof(float)));
+  FATE_CUDA(cudaMalloc(&al, ffn_alay_floats(max_off) * sizeof(float)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaError_t e = cudaMemcpyAsync(bd, bs.data(), sizeof(FfnBatch) * nsets, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_build_xlay(x_dev, H, xl, s);
+  for (int i = 0; i < nsets && e == cudaSuccess; ++i) e = launch_ffn_decode(bd + i, xl, al, y_dev, H, max_off, s);
+  if (e == cudaSuccess) e = cudaEventRecord(e0, s);
+  for (int i = 0; i < iters && e == cudaSuccess; ++i)
+    e = launch_ffn_decode(bd + (i % nsets), xl, al, y_dev, H, max_off, s);
+  if (e == cudaSuccess) e = cudaEventRecord(e1, s);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+  *ms_out = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(bd);
+  cudaFree(xl);
+  cudaFree(al);
+  FATE_CUDA(e);
   return FATE_OK;
 }

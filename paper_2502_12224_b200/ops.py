@@ -116,6 +116,22 @@ def ffn_decode(x: torch.Tensor, bufs: list, weights) -> torch.Tensor:
     return y
 
 
+def ffn_decode_timed(x: torch.Tensor, sets: list, weights, iters: int = 50):
+    """K3 launched `iters` times back to back cycling over expert `sets` (lists of
+    packed buffers of equal length); returns (y, mean kernel ms from CUDA events)."""
+    L = _lib.lib()
+    H = x.numel()
+    n, ns = len(sets[0]), len(sets)
+    flat = [b for s in sets for b in s]
+    arr = (C.c_void_p * len(flat))(*[ptr(b) for b in flat])
+    w = (C.c_float * n)(*[float(v) for v in weights])
+    y = torch.empty((H,), dtype=torch.float32, device=x.device)
+    ms = C.c_float(0.0)
+    check(L.fate_ffn_decode_timed(ptr(x.contiguous()), H, n, ns, arr, w, ptr(y), iters, _stream(), C.byref(ms)),
+          "fate_ffn_decode_timed")
+    return y, float(ms.value)
+
+
 def ffn_prefill(X: torch.Tensor, bufs: list, tok_lists: list, tok_weights: list) -> torch.Tensor:
     """K4 standalone: Y[t] = sum over experts e of w_{t,e} FFN_e(X[t]) for token lists per expert."""
     L = _lib.lib()

@@ -53,6 +53,73 @@ def k3(iters: int):
     print(json.dumps(out))
 
 
+def k3sweep(iters: int):
+    """K3 alone (fate_ffn_decode_timed) on expert sets of one format each and on
+    the Qwen mixes, cycling over enough copies of each set that the working set
+    exceeds 2x L2 (so every launch streams from HBM)."""
+    H, I, Is = 2048, 1408, 5632
+    g = torch.Generator(device="cuda").manual_seed(0)
+
+    def mk(I_, bits):
+        w = [torch.randn(sh, generator=g, device="cuda") * 0.02 for sh in ((I_, H), (I_, H), (H, I_))]
+        return ops.pack_expert(*w, bits)
+    x = torch.randn(H, device="cuda")
+    specs = {"bf16_shared": [(Is, 16)], "int4x4": [(I, 4)] * 4, "int2x4": [(I, 2)] * 4, "int8x4": [(I, 8)] * 4,
+             "qwen_mix_int4": [(I, 4)] * 4 + [(Is, 16)], "qwen_mix_int2": [(I, 2)] * 3 + [(I, 4), (Is, 16)],
+             "int4x12": [(I, 4)] * 12}
+    out = {}
+    only = os.environ.get("K3_ONLY")
+    for name, spec in specs.items():
+        if only and name != only:
+            continue
+        one = sum(make_layout_bytes(H, i, b) for i, b in spec)
+        nsets = max(2, min(64, int(np.ceil(300e6 / one))))
+        sets = [[mk(i, b) for i, b in spec] for _ in range(nsets)]
+        _, ms = ops.ffn_decode_timed(x, sets, [0.1] * len(spec), iters)
+        out[name] = {"ms": ms, "MB": one / 1e6, "gbs": one / (ms * 1e-3) / 1e9, "sets": nsets}
+        del sets
+        torch.cuda.empty_cache()
+        print(name, json.dumps(out[name]))
+        from paper_2502_12224_b200 import _lib
+        print_k3_trace(_lib)
+    print(json.dumps(out))
+
+
+def make_layout_bytes(H, I, bits):
+    n = 3 * H * I
+    return n * 2 if bits == 16 else n * bits // 8 + n // 64 * 8
+
+
+def print_k3_trace(_lib, mhz=1965.0):
+    buf = np.zeros(160 * 8 + 17 * 48 * 3 + 32, dtype=np.uint64)
+    _lib.load().fate_k3_profile(buf.ctypes.data)
+    prof = buf[:1280].reshape(160, 8)
+    P = prof[:148].astype(np.float64)
+    rel = (P - P[:, 0].min()) / 1000.0
+    names = ["start", "cons", "xlay", "phaseA", "gbar", "alay", "phaseB", "prod_done"]
+    print("K3 phase timestamps (us from first CTA start): median / max over CTAs")
+    for i, nm in enumerate(names):
+        print(f"  {nm:10s} {np.median(rel[:, i]):8.2f} {rel[:, i].max():8.2f}")
+    tr = buf[1280:1280 + 17 * 48 * 3].view(np.int64).reshape(17, 48, 3).astype(np.float64)
+    sub = buf[1280 + 17 * 48 * 3:].view(np.int64).reshape(8, 4).astype(np.float64)
+    nz = tr[tr > 0]
+    t0 = nz.min() if nz.size else 0.0
+    us = np.where(tr > 0, (tr - t0) / mhz, np.nan)
+    for t in range(8):
+        if sub[t, 0] > 0:
+            print(f"  sub tile {t}: dots done {(sub[t,0]-t0)/mhz:7.2f} sums {(sub[t,1]-t0)/mhz:7.2f} "
+                  f"store {(sub[t,2]-t0)/mhz:7.2f}")
+    print("CTA0 trace (us): producer [wait-start empty-passed issued] | consumer w1 [wait full released] | "
+          "max over consumers of release")
+    for t in range(48):
+        if np.all(np.isnan(us[:, t, :])):
+            break
+        rel_max = np.nanmax(us[1:, t, 2]) if not np.all(np.isnan(us[1:, t, 2])) else np.nan
+        full_min = np.nanmin(us[1:, t, 1]) if not np.all(np.isnan(us[1:, t, 1])) else np.nan
+        print(f"  {t:2d} P[{us[0,t,0]:6.2f} {us[0,t,1]:6.2f} {us[0,t,2]:6.2f}] "
+              f"C1[{us[1,t,0]:6.2f} {us[1,t,1]:6.2f} {us[1,t,2]:6.2f}] first_full {full_min:6.2f} last_rel {rel_max:6.2f}")
+
+
 def allhit(iters: int):
     from paper_2502_12224_b200.core import ModelConfig
     from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
@@ -72,23 +139,7 @@ def allhit(iters: int):
     wall = time.perf_counter() - t0
     st = res.stats
     from paper_2502_12224_b200 import _lib
-    buf = np.zeros(160 * 8 + 64 * 3, dtype=np.uint64)
-    _lib.load().fate_k3_profile(buf.ctypes.data)
-    prof = buf[:1280].reshape(160, 8)
-    tiles = buf[1280:].reshape(64, 3).astype(np.float64)
-    P = prof[:148].astype(np.float64)
-    t0 = P[:, 0].min()
-    rel = (P - t0) / 1000.0
-    names = ["start", "cons", "xlay", "phaseA", "gbar", "alay", "phaseB", "prod_done"]
-    print("K3 phase timestamps (us from first CTA start): median / max over CTAs")
-    for i, nm in enumerate(names):
-        print(f"  {nm:10s} {np.median(rel[:, i]):8.2f} {rel[:, i].max():8.2f}")
-    t00 = P[0, 0]
-    print("CTA0 tiles (us): issue / full seen (warp0) / released (warp0)")
-    for i in range(64):
-        if tiles[i, 0] == 0 and tiles[i, 1] == 0:
-            break
-        print(f"  {i:3d} {(tiles[i,0]-t00)/1e3:8.2f} {(tiles[i,1]-t00)/1e3:8.2f} {(tiles[i,2]-t00)/1e3:8.2f}")
+    print_k3_trace(_lib)
     k1 = np.zeros(8, dtype=np.uint64)
     _lib.load().fate_k1_profile(k1.ctypes.data)
     k1 = (k1.astype(np.float64) - float(k1[0])) / 1000.0
@@ -103,4 +154,4 @@ def allhit(iters: int):
 if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    {"k3": k3, "allhit": allhit}[mode](it)
+    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep}[mode](it)
