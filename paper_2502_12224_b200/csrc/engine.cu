@@ -856,6 +856,7 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
     FATE_CUDA(cudaFuncGetAttributes(&fa, run_begin_kernel));
     FATE_CUDA(ffn_preload());
     FATE_CUDA(k4_preload());
+    FATE_CUDA(k4_tc_preload());
     FATE_CUDA(gate_preload());
     if (int st = prefill_preload()) return st;
   }
@@ -1367,6 +1368,7 @@ struct PfScratch {
   int32_t *order;    // [T, E] layer l
   int32_t *order_n;  // [T, E] layer l+1
   float *X;          // [T, H]
+  __nv_bfloat16 *Xb; // [T, H] the same rows in bf16 (K4 operand)
   int32_t *chosen;   // [T, k] ascending
   float *cw;         // [T, k]
   int32_t *tok_idx;  // [T*(k+1)]
@@ -1380,12 +1382,15 @@ struct PfScratch {
   float *Z;
 };
 
-__global__ void prefill_x_kernel(const double *gate_in, int T, int L, int layer, int H, float *X) {
+__global__ void prefill_x_kernel(const double *gate_in, int T, int L, int layer, int H, float *X,
+                                 __nv_bfloat16 *Xb) {
   const double sH = sqrt((double)H);
   const int64_t n = (int64_t)T * H;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / H, h = i % H;
-    X[i] = (float)(sH * gate_in[(t * L + layer) * H + h]);
+    const float x = (float)(sH * gate_in[(t * L + layer) * H + h]);
+    X[i] = x;
+    Xb[i] = __float2bfloat16_rn(x);
   }
 }
 
@@ -1697,7 +1702,7 @@ static int ensure_prefill_scratch(fate_engine *g, PfScratch &s, int T) {
     return o;
   };
   const size_t o_r = carve((size_t)Tm * E * 8), o_o = carve((size_t)Tm * E * 4), o_on = carve((size_t)Tm * E * 4),
-               o_x = carve((size_t)Tm * H * 4), o_c = carve((size_t)Tm * k * 4), o_cw = carve((size_t)Tm * k * 4),
+               o_x = carve((size_t)Tm * H * 4), o_xb = carve((size_t)Tm * H * 2), o_c = carve((size_t)Tm * k * 4), o_cw = carve((size_t)Tm * k * 4),
                o_ti = carve((size_t)Tm * (k + 1) * 4), o_zr = carve((size_t)Tm * (k + 1) * 4),
                o_ex = carve(sizeof(PrefillExpert) * (E + 1)), o_ao = carve(4 * (E + 1)), o_st = carve(4 * E),
                o_ac = carve(4 * E), o_v = carve(4 * (size_t)L * (E + 1)), o_si = carve(16),
@@ -1708,6 +1713,7 @@ static int ensure_prefill_scratch(fate_engine *g, PfScratch &s, int T) {
   s.order = (int32_t *)(b + o_o);
   s.order_n = (int32_t *)(b + o_on);
   s.X = (float *)(b + o_x);
+  s.Xb = (__nv_bfloat16 *)(b + o_xb);
   s.chosen = (int32_t *)(b + o_c);
   s.cw = (float *)(b + o_cw);
   s.tok_idx = (int32_t *)(b + o_ti);
@@ -1775,7 +1781,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   FATE_CUDA(cudaMemcpy(tau.data(), g->d.tau, L * 8, cudaMemcpyDeviceToHost));
   auto launch_front = [&](int l) -> int {
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l], cs));
-    prefill_x_kernel<<<148 * 4, 256, 0, cs>>>(gate_in_dev, T, L, l, H, s.X);
+    prefill_x_kernel<<<148 * 4, 256, 0, cs>>>(gate_in_dev, T, L, l, H, s.X, s.Xb);
     FATE_CHECK_LAUNCH("prefill_x_kernel");
     FATE_CUDA(launch_gate_batch(g->d.W + (int64_t)l * E * H, tau[l], gate_in_dev + (int64_t)l * H, (int64_t)L * H, T,
                                 E, H, s.routing, s.order, nullptr, k, 0, 0.5, cs));
@@ -1904,19 +1910,19 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l + 2], cs));
     int tiles_up = 0, tiles_down = 0;
     for (int i = 0; i < m.n_active; ++i) {
-      tiles_up += k4_tiles(m.active_cnt[i], I, H, false);
-      tiles_down += k4_tiles(m.active_cnt[i], I, H, true);
+      tiles_up += k4_tc_items(m.active_cnt[i], I, H, false);
+      tiles_down += k4_tc_items(m.active_cnt[i], I, H, true);
       flops += 6.0 * H * I * m.active_cnt[i];
     }
     int n_ex = m.n_active;
     const int has_shared = g->cfg.shared_intermediate && g->shared_dev[l] ? 1 : 0;
     if (has_shared) {
-      tiles_up += k4_tiles(T, g->cfg.shared_intermediate, H, false);
-      tiles_down += k4_tiles(T, g->cfg.shared_intermediate, H, true);
+      tiles_up += k4_tc_items(T, g->cfg.shared_intermediate, H, false);
+      tiles_down += k4_tc_items(T, g->cfg.shared_intermediate, H, true);
       flops += 6.0 * H * g->cfg.shared_intermediate * T;
       ++n_ex;
     }
-    FATE_CUDA(launch_k4_simt(s.X, H, s.ex, n_ex, s.tok_idx, s.zrow, s.a_off, s.A, s.Z, tiles_up, tiles_down, cs));
+    FATE_CUDA(launch_k4_tc(s.Xb, H, s.ex, n_ex, s.tok_idx, s.zrow, s.a_off, s.A, s.Z, tiles_up, tiles_down, cs));
     FATE_CUDA(launch_k4_combine(s.Z, s.cw, T, k, H, has_shared, Y_dev + (int64_t)l * T * H, cs));
     prefill_arc_kernel<<<1, 32, 0, cs>>>(d, s, l, m.n_active);
     FATE_CHECK_LAUNCH("prefill_arc_kernel");

@@ -160,13 +160,15 @@ struct PrefillExpert {
   int n_tok;
 };
 
-cudaError_t launch_k4_simt(const float *X, int H, const PrefillExpert *ex_dev, int n, const int32_t *tok_idx,
-                           const int32_t *zrow, const int *a_off_dev, float *A, float *Z, int tiles_up,
-                           int tiles_down, cudaStream_t s);
 cudaError_t launch_k4_combine(const float *Z, const float *w, int T, int k, int H, int has_shared, float *Y,
                               cudaStream_t s);
 cudaError_t k4_preload();
+// K4 on tcgen05 (prefill_tc.cu): Xb bf16 token rows [T, H], A bf16 activations, Z fp32 rows.
+cudaError_t launch_k4_tc(const void *Xb, int H, const PrefillExpert *ex_dev, int n, const int32_t *tok_idx,
+                         const int32_t *zrow, const int *a_off_dev, void *A, float *Z, int items_up, int items_down,
+                         cudaStream_t s);
+cudaError_t k4_tc_preload();
+int k4_tc_items(int n_tok, int I, int H, bool down);
 cudaError_t gate_preload();
-int k4_tiles(int n_tok, int I, int H, bool down);
 
 }  // namespace fate

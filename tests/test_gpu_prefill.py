@@ -16,7 +16,10 @@ from oracle import fate_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-Y_REL_L2 = 2e-5
+# K4 runs on tcgen05 with bf16 operands (token rows and dequantized weights
+# rounded to bf16) and fp32 accumulation: stated tolerance against the fp64
+# oracle on the same packed weights.
+Y_REL_L2 = 1e-2
 
 
 def _setup(name, shared=0, n=15):
@@ -97,6 +100,7 @@ def test_prefill_outputs_match_fp64_oracle():
                 d = deq[int(a)]
                 want = want + np.float32(r[a]) * O.ffn_swiglu(x, d["w1"], d["w3"], d["w2"])
             worst = max(worst, np.linalg.norm(Y[l, t] - want) / np.linalg.norm(want))
+    print(f"prefill Y worst rel-L2 vs fp64 oracle: {worst:.3e}")
     assert worst <= Y_REL_L2, worst
     eng.close()
 
@@ -122,4 +126,37 @@ def test_ffn_prefill_standalone():
         for t, wv in zip(tl, wl):
             want[t] += wv * O.ffn_swiglu(Xd[t], r["w1"], r["w3"], r["w2"])
     rel = np.linalg.norm(Y - want) / np.linalg.norm(want)
+    print(f"ffn_prefill rel-L2 vs fp64 oracle: {rel:.3e}")
     assert rel <= Y_REL_L2, rel
+
+
+def test_ffn_prefill_qwen_shape_multi_tile():
+    # Qwen expert geometry, token lists longer than one 128-token tile, mixed widths
+    import torch
+    from paper_2502_12224_b200 import ops
+    H, I = 2048, 1408
+    g = torch.Generator(device="cuda").manual_seed(11)
+    bufs, refs = [], []
+    for b in (4, 2, 16, 8):
+        ws = [torch.randn(s, generator=g, device="cuda") * 0.02 for s in ((I, H), (I, H), (H, I))]
+        buf = ops.pack_expert(*ws, b)
+        bufs.append(buf)
+        refs.append(O.unpack_buffer(buf.cpu().numpy(), H, I, b))
+    T = 300
+    X = torch.randn((T, H), generator=g, device="cuda")
+    rng = np.random.default_rng(3)
+    toks = [sorted(rng.choice(T, size=n, replace=False).tolist()) for n in (300, 130, 17, 1)]
+    wts = [rng.uniform(0.05, 1.0, size=len(tl)).tolist() for tl in toks]
+    Y = ops.ffn_prefill(X, bufs, toks, wts).cpu().numpy().astype(np.float64)
+    Xd = X.cpu().numpy().astype(np.float64)
+    want = np.zeros((T, H))
+    for r, tl, wl in zip(refs, toks, wts):
+        h1, h3 = Xd[tl] @ r["w1"].T, Xd[tl] @ r["w3"].T
+        a = h1 / (1.0 + np.exp(-h1)) * h3
+        want[tl] += np.asarray(wl)[:, None] * (a @ r["w2"].T)
+    rel = np.linalg.norm(Y - want) / np.linalg.norm(want)
+    print(f"ffn_prefill qwen-shape rel-L2 vs fp64 oracle: {rel:.3e}")
+    assert rel <= Y_REL_L2, rel
+    # every listed token row got its contribution (no dropped tiles)
+    row_rel = np.linalg.norm(Y - want, axis=1) / np.maximum(np.linalg.norm(want, axis=1), 1e-30)
+    assert row_rel.max() <= 5 * Y_REL_L2, row_rel.max()

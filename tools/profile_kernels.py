@@ -120,6 +120,47 @@ def print_k3_trace(_lib, mhz=1965.0):
               f"C1[{us[1,t,0]:6.2f} {us[1,t,1]:6.2f} {us[1,t,2]:6.2f}] first_full {full_min:6.2f} last_rel {rel_max:6.2f}")
 
 
+def prefill(tokens: int):
+    """DeepSeek-MoE-16B shape prefill (BASELINE configs[2]): 28 layers, 64 experts
+    top-6 + shared 2 x 1408 (as one 2816 expert, bf16), T tokens; (a) every expert
+    resident (pure K4 tensor-core time), (b) 448 INT4 slots cold (the bench case)."""
+    from paper_2502_12224_b200.core import ModelConfig
+    from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
+    from paper_2502_12224_b200.experts import ExpertStore
+    from paper_2502_12224_b200.gatesim import GenConfig, gen_trace
+    from paper_2502_12224_b200.cache import plan_allocation
+    cfg = ModelConfig.from_shape(28, 64, 6, 2048, 1408, 3, dense_bytes=28 * 3 * 2048 * 2816 * 2)
+    tr, w = gen_trace(cfg, GenConfig(seed=0, num_tokens=tokens, phase="prefill"))
+    store = ExpertStore(cfg, bits=(4, 2), shared_intermediate=2816, shared_bits=16)
+    _, g, ch = tr.dense_arrays(cfg)
+    gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
+    out = {}
+    for mode in ("allhit", "cold448"):
+        if mode == "allhit":
+            caps = [64] * 28
+        else:
+            caps = list(plan_allocation(cfg, cfg.dense_bytes + 448 * cfg.expert_bytes[4], 4).per_layer_capacity)
+        eng = OffloadEngine(cfg, caps, store, w, StrategyKnobs(budget_n=0), max_tokens=max(tokens, 64))
+        if mode == "allhit":
+            for l in range(28):
+                eng.seed_resident(l, range(64))
+        eng.prefill(gd, chd)
+        if mode == "allhit":
+            for l in range(28):
+                eng.seed_resident(l, range(64))
+        else:
+            eng.reset_cache()
+        t0 = time.perf_counter()
+        Y, st, logs, step_ms, copies = eng.prefill(gd, chd)
+        wall = time.perf_counter() - t0
+        out[mode] = {"gpu_ms": st["gpu_ms"], "tok_s": tokens / st["gpu_ms"] * 1e3, "k4_ms": st["ffn_ms"],
+                     "k4_tflops": st["ffn_flops"] / (st["ffn_ms"] * 1e-3) / 1e12, "wall_s": wall,
+                     "h2d_gb": st["h2d_bytes"] / 1e9}
+        eng.close()
+        print(mode, json.dumps(out[mode]), flush=True)
+    print(json.dumps(out))
+
+
 def allhit(iters: int):
     from paper_2502_12224_b200.core import ModelConfig
     from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
@@ -154,4 +195,4 @@ def allhit(iters: int):
 if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep}[mode](it)
+    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill}[mode](it)
