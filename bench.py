@@ -168,6 +168,52 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 
+DSK = dict(L=28, E=64, k=6, H=2048, I=1408, Lb=3, shared=2816, slots=448, tokens=512)
+
+
+def bench_prefill(peaks, rank: int) -> dict:
+    """BASELINE configs[2]: DeepSeek-MoE-16B shape prefill of 512 tokens with a
+    448-slot INT4 expert cache (25% of 1792), cold cache, Strategy.fate() prefill
+    path (pipeline.simulate_prefill semantics on the device engine)."""
+    import torch
+    from paper_2502_12224_b200 import pipeline as P
+    from paper_2502_12224_b200.cache import plan_allocation
+    from paper_2502_12224_b200.core import ModelConfig
+    from paper_2502_12224_b200.engine import OffloadEngine
+    from paper_2502_12224_b200.experts import ExpertStore
+    from paper_2502_12224_b200.gatesim import GenConfig, gen_trace
+    c = DSK
+    cfg = ModelConfig.from_shape(c["L"], c["E"], c["k"], c["H"], c["I"], c["Lb"],
+                                 dense_bytes=c["L"] * 3 * c["H"] * c["shared"] * 2)
+    tr, w = gen_trace(cfg, GenConfig(seed=rank, num_tokens=c["tokens"], phase="prefill"))
+    store = ExpertStore(cfg, bits=(4, 2), seed=rank, shared_intermediate=c["shared"], shared_bits=16)
+    plan = plan_allocation(cfg, cfg.dense_bytes + c["slots"] * cfg.expert_bytes[4], 4)
+    strategy = P.Strategy.fate()
+    _, g, ch = tr.dense_arrays(cfg)
+    gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
+    eng = OffloadEngine(cfg, plan.per_layer_capacity, store, w, P.knobs_for(strategy, plan, 0),
+                        max_tokens=c["tokens"])
+    eng.prefill(gd, chd)  # warm-up (kernel load, pools)
+    runs = []
+    for _ in range(2):
+        eng.reset_cache()
+        _, st, _, _, _ = eng.prefill(gd, chd)
+        runs.append(st)
+    eng.close()
+    st = min(runs, key=lambda r: r["gpu_ms"])
+    k4_tflops = st["ffn_flops"] / (st["ffn_ms"] * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops", 1667.9)
+    return {"workload": "DeepSeek-MoE-16B shape prefill 512 tokens, 448 INT4 slots, cold (BASELINE configs[2])",
+            "tokens_per_s": c["tokens"] / st["gpu_ms"] * 1e3, "ms": st["gpu_ms"],
+            "h2d_gbs": st["h2d_bytes"] / (st["copy_busy_ms"] * 1e-3) / 1e9 if st["copy_busy_ms"] else None,
+            "h2d_bytes": st["h2d_bytes"],
+            "roofline": {"bound": "tensor", "kernel": "K4 tcgen05 grouped SwiGLU (up + down)",
+                         "achieved": k4_tflops, "peak": peak, "unit": "TFLOP/s", "frac": k4_tflops / peak,
+                         "flops": st["ffn_flops"], "k4_ms": st["ffn_ms"],
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+            "dtype": "bf16 operands (dequantized INT4/INT2 experts, bf16 shared), fp32 accumulate"}
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "r01_k3_ncu.json")
     if os.path.exists(p):
@@ -189,6 +235,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-prefill", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -305,6 +352,12 @@ def main():
         cpu = {"value": args.cpu_tokens / secs, "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"first {args.cpu_tokens} tokens of the same trace, 24 layers (fp64 gate + top-4 + "
                          "dequant-fused INT4 routed + bf16 shared FFN, C threads over rows)"}
+    pre = None
+    if not args.no_prefill:
+        eng.close()
+        eng = None
+        torch.cuda.empty_cache()
+        pre = bench_prefill(peaks, rank)
     if rank == 0:
         clocks = clk.summary()
         out = {
@@ -336,10 +389,12 @@ def main():
                     "ondemand": agg["ondemand_issued"], "prefetch": agg["prefetch_issued"]},
             "k1_ms_per_launch": agg["gate_ms"] / agg["steps"],
             "trace_mismatches": agg["trace_mismatches"],
+            "prefill": pre,
             "wall_s_timed": wall,
         }
         print(json.dumps(out), flush=True)
-    eng.close()
+    if eng is not None:
+        eng.close()
     if world > 1:
         dist.destroy_process_group()
 

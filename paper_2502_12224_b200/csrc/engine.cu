@@ -1119,8 +1119,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   FATE_CHECK_LAUNCH("run_begin_kernel");
   FATE_CUDA(cudaStreamSynchronize(cs));
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] run_begin done\n");
-  int launched = 0, processed = 0;
+  int launched = 0, processed = 0, k3_next = 0;
   const int lookahead = 4;
+  const bool serial = getenv("FATE_PROFILE_SERIAL") != nullptr;
   int status = FATE_OK;
   auto last_progress = std::chrono::steady_clock::now();
   const int rows_pred = g->cfg.use_predictor ? 2 : 1;
@@ -1133,8 +1134,33 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
               processed, launched, ch.pending.size(), ch.inflight.size(), ch.submitted, *g->copy_done_host,
               g->ring_host[processed % kRing].seq);
     }
+    // profiling mode (FATE_PROFILE_SERIAL, e.g. under ncu, which serializes
+    // launches): K3 of a step is enqueued only after the host has serviced that
+    // step's message and submitted its transfers, so the launch never blocks on
+    // a stream wait that this thread itself must release.  Same decisions and
+    // results; only the overlap is lost.
+    while (serial && k3_next < launched && k3_next < processed) {
+      const int s = k3_next, t = s / L, l = s % L;
+      // every transfer this step needs has landed (the flag the stream waits on)
+      while (((volatile uint32_t *)g->ready_host)[l] < (uint32_t)t + 1u) {
+        if ((status = ch.pump())) break;
+        _mm_pause();
+        if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(30)) {
+          status = FATE_ETIMEOUT;
+          set_error("fate_engine_decode: transfers of a step never completed (serial mode)");
+          break;
+        }
+      }
+      if (status) break;
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+      FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                         g->max_total_I, &g->d.stats->ffn_bytes, cs));
+      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+      ++k3_next;
+    }
+    if (status) break;
     // enqueue compute for steps up to `lookahead` beyond the host's progress
-    while (launched < n_steps && launched < processed + lookahead) {
+    while (launched < n_steps && launched < processed + (serial ? 1 : lookahead) && (!serial || k3_next == launched)) {
       const int s = launched, t = s / L, l = s % L;
       // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
       const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
@@ -1147,10 +1173,12 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
                                   CU_STREAM_WAIT_VALUE_GEQ));
       if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
-      FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                         g->max_total_I, &g->d.stats->ffn_bytes, cs));
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+      if (!serial) {
+        if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+        FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                           g->max_total_I, &g->d.stats->ffn_bytes, cs));
+        if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+      }
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K3 step %d\n", s);
       ++launched;
     }
@@ -1239,6 +1267,15 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
       break;
     }
+  }
+  // profiling mode: the last step's K3 (its transfers were drained above)
+  while (status == FATE_OK && serial && k3_next < launched) {
+    const int s = k3_next, t = s / L, l = s % L;
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+    FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                       g->max_total_I, &g->d.stats->ffn_bytes, cs));
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+    ++k3_next;
   }
   arc_flush_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
   cudaError_t fe = cudaGetLastError();

@@ -91,7 +91,9 @@ def launch(csv_path, out):
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
-                v = float(d["Metric Value"].replace(",", "")) * (1e-3 if d.get("Metric Unit") == "nsecond" else 1.0)
+                u = d.get("Metric Unit", "")
+                v = float(d["Metric Value"].replace(",", "")) * (1e-3 if u in ("ns", "nsecond") else
+                                                                  1e3 if u in ("ms", "msecond") else 1.0)
                 agg[d["Kernel Name"].split("(")[0][:90]].append(v)
     tot = sum(sum(v) for v in agg.values())
     res = [{"kernel": k, "launches": len(v), "mean_us": sum(v) / len(v), "share": sum(v) / tot}
