@@ -321,7 +321,21 @@ def main():
     k3_ms = agg["ffn_ms"] / k3_launches
     k3_bytes = agg["ffn_bytes"] / k3_launches
     achieved = k3_bytes / (k3_ms * 1e-3) / 1e9
-    h2d_gbs = agg["h2d_bytes"] / (agg["copy_busy_ms"] * 1e-3) / 1e9 if agg["copy_busy_ms"] else None
+    # H2D GB/s over the union of the copy intervals of the last timed step (two copy
+    # streams overlap, so summed per-copy durations would undercount the rate)
+    _, copies_tl = eng.timeline()
+    h2d_gbs = None
+    if copies_tl:
+        iv = sorted((a, b) for (a, b, *_r) in copies_tl)
+        busy, cur_a, cur_b = 0.0, iv[0][0], iv[0][1]
+        for a, b in iv[1:]:
+            if a > cur_b:
+                busy += cur_b - cur_a
+                cur_a, cur_b = a, b
+            else:
+                cur_b = max(cur_b, b)
+        busy += cur_b - cur_a
+        h2d_gbs = stats[-1]["h2d_bytes"] / (busy * 1e-3) / 1e9 if busy > 0 else None
 
     # -- e2e through the public API: host GateTrace in, last-layer outputs back to host
     e2e_times, h2d_b, d2h_b = [], 0, 0

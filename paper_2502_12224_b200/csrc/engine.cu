@@ -633,7 +633,9 @@ struct Transfer {
 struct Inflight {
   uint32_t seq;
   Transfer t;
-  int ev;  // index of the start/stop event pair (-1 untimed)
+  int ev;       // index of the start/stop event pair (-1 untimed)
+  int stream;   // copy stream (0/1) it was submitted on
+  uint32_t sseq;  // per-stream completion sequence number
 };
 
 struct fate_engine {
@@ -651,15 +653,16 @@ struct fate_engine {
   StepMsg *ring_host = nullptr;
   volatile uint32_t *ready_host = nullptr;     // [L]
   uint32_t *ready_dev = nullptr;
-  volatile uint32_t *copy_done_host = nullptr;
-  CUdeviceptr copy_done_dev = 0;
+  volatile uint32_t *copy_done_host = nullptr, *copy_done_host2 = nullptr;  // per copy stream
+  CUdeviceptr copy_done_dev = 0, copy_done_dev2 = 0;
   // host pools
   const uint8_t *host_pool[17] = {};
   int64_t host_stride[17] = {};
   std::vector<const uint8_t *> shared_dev;
   const uint8_t **shared_table_dev = nullptr;
   int32_t *pf_shared_I = nullptr;
-  cudaStream_t cstream = nullptr, xstream = nullptr;
+  cudaStream_t cstream = nullptr, xstream = nullptr, xstream2 = nullptr;  // compute, two copy streams
+  cudaEvent_t xlast[2] = {nullptr, nullptr};  // last copy submitted on each copy stream
   int max_total_I = 0;
   int prefill_max_tokens = 0;
   // prefill scratch
@@ -838,13 +841,17 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   memset(p, 0, 4096);
   g->ready_host = (volatile uint32_t *)p;
   g->copy_done_host = (volatile uint32_t *)((uint8_t *)p + 2048);
+  g->copy_done_host2 = (volatile uint32_t *)((uint8_t *)p + 2176);
   FATE_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
   g->ready_dev = (uint32_t *)pd;
   g->copy_done_dev = (CUdeviceptr)((uint8_t *)pd + 2048);
+  g->copy_done_dev2 = (CUdeviceptr)((uint8_t *)pd + 2176);
   int lo = 0, hi = 0;
   FATE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   FATE_CUDA(cudaStreamCreateWithPriority(&g->cstream, cudaStreamNonBlocking, hi));
   FATE_CUDA(cudaStreamCreateWithPriority(&g->xstream, cudaStreamNonBlocking, lo));
+  FATE_CUDA(cudaStreamCreateWithPriority(&g->xstream2, cudaStreamNonBlocking, lo));
+  for (auto &e : g->xlast) FATE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // load every kernel the engine launches now: lazy module loading at first
   // launch can deadlock behind a stream parked on a cuStreamWaitValue32 flag
   {
@@ -871,8 +878,12 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   if (!g) return FATE_OK;
   cudaStreamSynchronize(g->cstream);
   cudaStreamSynchronize(g->xstream);
+  if (g->xstream2) cudaStreamSynchronize(g->xstream2);
   cudaStreamDestroy(g->cstream);
   cudaStreamDestroy(g->xstream);
+  if (g->xstream2) cudaStreamDestroy(g->xstream2);
+  for (auto &e : g->xlast)
+    if (e) cudaEventDestroy(e);
   cudaFree(g->pool);
   cudaFree(g->dev_block);
   if (g->pf_block) cudaFree(g->pf_block);
@@ -1002,10 +1013,20 @@ struct Channel {
 
   int bytes_of(int bits) const { return (int)buffer_bytes(g->cfg.hidden_dim, g->cfg.intermediate_dim, bits); }
 
+  uint32_t submitted_s[2] = {0u, 0u};
+  int next_stream = 0;
+
+  // Transfers alternate between two copy streams (two DMA engines), in the
+  // channel's FIFO submission order; the completion of each stream is a
+  // per-stream counter written behind its copies.  A step's wait flag is
+  // written on the stream of the last transfer the step needs, after waiting
+  // for the other stream's last copy, so it still follows every one of them.
   int submit_one(const Transfer &t) {
-    const cudaStream_t s = g->xstream;
+    const int si = t.kind == 2 ? 0 : next_stream;
+    const cudaStream_t s = si ? g->xstream2 : g->xstream;
     int evi = -1;
     if (t.kind != 2) {
+      next_stream ^= 1;
       if (!g->host_pool[t.bits]) {
         set_error("no pinned host pool registered for a requested bit width");
         return FATE_EINVAL;
@@ -1019,18 +1040,28 @@ struct Channel {
       }
       FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)t.buf * g->buf_stride, src, bytes, cudaMemcpyHostToDevice, s));
       if (evi >= 0) FATE_CUDA(cudaEventRecord(ev[evi + 1], s));
-      FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
+      // landed marks are read only for queued prefetches (K1's arrival check):
+      // on-demand copies skip the extra stream op between back-to-back copies
+      if (t.kind == 0) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
+      FATE_CUDA(cudaEventRecord(g->xlast[si], s));
       h2d_bytes += bytes;
     }
+    // the step's wait flag is released by the copy streams themselves right
+    // after the last transfer the step needs (the host also sets it when reaping)
+    if (t.signal_token >= 0) {
+      FATE_CUDA(cudaStreamWaitEvent(s, g->xlast[si ^ 1], 0));
+      FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->ready_dev + t.signal_layer), (uint32_t)t.signal_token + 1u, 0));
+    }
     ++submitted;
-    FATE_CU(p_write32((CUstream)s, g->copy_done_dev, submitted, 0));
-    inflight.push_back(Inflight{submitted, t, evi});
+    const uint32_t sseq = ++submitted_s[si];
+    FATE_CU(p_write32((CUstream)s, si ? g->copy_done_dev2 : g->copy_done_dev, sseq, 0));
+    inflight.push_back(Inflight{submitted, t, evi, si, sseq});
     return FATE_OK;
   }
 
   void reap() {
-    const uint32_t c = *g->copy_done_host;
-    while (!inflight.empty() && (int32_t)(c - inflight.front().seq) >= 0) {
+    const uint32_t c[2] = {*g->copy_done_host, *g->copy_done_host2};
+    while (!inflight.empty() && (int32_t)(c[inflight.front().stream] - inflight.front().sseq) >= 0) {
       Inflight &f = inflight.front();
       if (f.ev >= 0) {
         float ms = 0.f;
@@ -1112,6 +1143,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   g->copy_meta.clear();
   for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
   *g->copy_done_host = 0;
+  *g->copy_done_host2 = 0;
   for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
   const cudaStream_t cs = g->cstream;
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
@@ -1122,6 +1154,15 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   int launched = 0, processed = 0, k3_next = 0;
   const int lookahead = 4;
   const bool serial = getenv("FATE_PROFILE_SERIAL") != nullptr;
+  // K3 of step s (routed + shared experts), after the step's wait
+  auto ffn_step = [&](int s) -> int {
+    const int t = s / L, l = s % L;
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+    FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                       g->max_total_I, &g->d.stats->ffn_bytes, 0, cs));
+    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+    return FATE_OK;
+  };
   int status = FATE_OK;
   auto last_progress = std::chrono::steady_clock::now();
   const int rows_pred = g->cfg.use_predictor ? 2 : 1;
@@ -1152,10 +1193,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         }
       }
       if (status) break;
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
-      FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                         g->max_total_I, &g->d.stats->ffn_bytes, cs));
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+      if ((status = ffn_step(s))) break;
       ++k3_next;
     }
     if (status) break;
@@ -1173,12 +1211,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
                                   CU_STREAM_WAIT_VALUE_GEQ));
       if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
-      if (!serial) {
-        if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
-        FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                           g->max_total_I, &g->d.stats->ffn_bytes, cs));
-        if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
-      }
+      if (!serial && (status = ffn_step(s))) break;
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K3 step %d\n", s);
       ++launched;
     }
@@ -1270,17 +1303,14 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   }
   // profiling mode: the last step's K3 (its transfers were drained above)
   while (status == FATE_OK && serial && k3_next < launched) {
-    const int s = k3_next, t = s / L, l = s % L;
-    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
-    FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                       g->max_total_I, &g->d.stats->ffn_bytes, cs));
-    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+    if ((status = ffn_step(k3_next))) break;
     ++k3_next;
   }
   arc_flush_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
   cudaError_t fe = cudaGetLastError();
   cudaError_t se = cudaStreamSynchronize(cs);
   cudaError_t xe = cudaStreamSynchronize(g->xstream);
+  if (xe == cudaSuccess) xe = cudaStreamSynchronize(g->xstream2);
   if (status == FATE_OK && fe != cudaSuccess) status = cuda_status(fe, "arc_flush_kernel");
   if (status == FATE_OK && se != cudaSuccess) status = cuda_status(se, "decode compute stream");
   if (status == FATE_OK && xe != cudaSuccess) status = cuda_status(xe, "decode copy stream");
@@ -1806,6 +1836,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   g->copy_meta.clear();
   for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
   *g->copy_done_host = 0;
+  *g->copy_done_host2 = 0;
   for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
   EngineDev d = g->d;
   d.ready = g->ready_dev;
@@ -1984,6 +2015,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
     }
   }
   cudaError_t se = cudaStreamSynchronize(cs), xe = cudaStreamSynchronize(g->xstream);
+  if (xe == cudaSuccess) xe = cudaStreamSynchronize(g->xstream2);
   if (status == FATE_OK && se != cudaSuccess) status = cuda_status(se, "prefill compute stream");
   if (status == FATE_OK && xe != cudaSuccess) status = cuda_status(xe, "prefill copy stream");
   DevStats ds{};

@@ -161,6 +161,60 @@ def prefill(tokens: int):
     print(json.dumps(out))
 
 
+def timeline(tokens: int):
+    """Per-step critical path of the bench decode (Qwen shape, 360 INT4 slots, cold):
+    K1, K1 end -> first copy start, copy span, last copy end -> K3 start, K3, K3 end ->
+    next K1 (all from the engine's CUDA events, ms relative to the run start)."""
+    sys.path.insert(0, ROOT)
+    import bench as B
+    from paper_2502_12224_b200 import pipeline as P
+    from paper_2502_12224_b200.cache import plan_allocation
+    from paper_2502_12224_b200.engine import OffloadEngine
+    from paper_2502_12224_b200.experts import ExpertStore
+    cfg = B.qwen_cfg()
+    trace, weights = B.make_trace(cfg, tokens, 0)
+    store = ExpertStore(cfg, bits=(4, 2), seed=0, shared_intermediate=B.QWEN["shared"], shared_bits=16)
+    plan = plan_allocation(cfg, cfg.dense_bytes + B.QWEN["slots"] * cfg.expert_bytes[4], 4)
+    _, g, ch = trace.dense_arrays(cfg)
+    gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
+    eng = OffloadEngine(cfg, plan.per_layer_capacity, store, weights, P.knobs_for(P.Strategy.fate(), plan, 0),
+                        max_tokens=max(tokens, 64))
+    eng.decode(gd, chd)
+    eng.reset_cache()
+    res = eng.decode(gd, chd)
+    sm, copies = eng.timeline()
+    n = sm.shape[0]
+    by_step = {}
+    for (a, b, kind, step, layer, e, bits) in copies:
+        by_step.setdefault(step * cfg.num_layers + layer if False else None, None)
+    # copies carry (token, layer): map to the flat step index
+    cs = {}
+    for (a, b, kind, tok, layer, e, bits) in copies:
+        cs.setdefault(tok * cfg.num_layers + layer, []).append((a, b, kind))
+    rows = []
+    for s in range(n):
+        k1a, k1b, k3a, k3b = sm[s]
+        c = cs.get(s, [])
+        od = [x for x in c if x[2] == 1]
+        first = min((x[0] for x in od), default=np.nan)
+        last = max((x[1] for x in od), default=np.nan)
+        nxt = sm[s + 1][0] if s + 1 < n else np.nan
+        rows.append([k1b - k1a, first - k1b, last - first, k3a - last if od else k3a - k1b, k3b - k3a, nxt - k3b,
+                     len(od)])
+    for s_ in (300, 301, 302):
+        print("step", s_, "K1 %.1f-%.1f K3 %.1f-%.1f" % tuple(1e3 * x for x in sm[s_]),
+              "copies", [("%.1f-%.1f k%d e%d b%d" % (1e3 * a, 1e3 * b, kd, e, bt))
+                         for (a, b, kd, tok, layer, e, bt) in copies if tok * cfg.num_layers + layer == s_])
+    R = np.array(rows) * np.array([1e3] * 6 + [1])
+    names = ["K1", "K1end->copy0", "copy span", "copyN->K3", "K3", "K3end->nextK1", "n_od"]
+    med = np.nanmedian(R, axis=0)
+    mean = np.nanmean(R, axis=0)
+    print(json.dumps({"steps": n, "tok_s": tokens / res.stats["gpu_ms"] * 1e3,
+                      "median_us": dict(zip(names, [round(float(v), 2) for v in med])),
+                      "mean_us": dict(zip(names, [round(float(v), 2) for v in mean])),
+                      "step_us_mean": float((sm[-1][3] - sm[0][0]) / n * 1e3)}))
+
+
 def allhit(iters: int):
     from paper_2502_12224_b200.core import ModelConfig
     from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
@@ -195,4 +249,4 @@ def allhit(iters: int):
 if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill}[mode](it)
+    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline}[mode](it)
