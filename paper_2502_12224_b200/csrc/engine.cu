@@ -150,7 +150,7 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
 // K1 phase timestamps of the last launch (globaltimer ns), diagnostics only:
 // [0] block 0 start, [1] tail start, [2] state staged, [3] routed, [4] split,
 // [5] predicted, [6] message posted
-__device__ unsigned long long g_k1_prof[8];
+__device__ unsigned long long g_k1_prof[16];
 
 __device__ __forceinline__ unsigned long long gtime1() {
   unsigned long long t;
@@ -159,7 +159,6 @@ __device__ __forceinline__ unsigned long long gtime1() {
 }
 
 struct TailSmem {
-  ArcLayer arc;
   int32_t bof_l[EMAX], pend_l[EMAX], bof_n[EMAX], bbits_l[EMAX];
   uint32_t pgen_l[EMAX], pdone_l[EMAX];
   int32_t pred_prev[EMAX];
@@ -167,7 +166,6 @@ struct TailSmem {
   double z[2 * EMAX], w[2 * EMAX];
   int32_t ord[2 * EMAX];
   int32_t chosen[KMAX], cbuf[KMAX], csrc[KMAX], chit[KMAX], carr[KMAX];
-  int32_t rel[4 * KMAX + 4];
   int32_t is_chosen[EMAX];
   alignas(16) float xs[4096];  // x = sqrt(H) * gate_in, H <= 4096 (float4-read by write_xlay)
 };
@@ -183,14 +181,14 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   const double *h = gate_in + ((int64_t)token * L + layer) * H;
   // block 0: the tail (stages state while the others work), blocks
   // 1..n_rows: router rows, last block: the deferred ARC update
-  const int n_rows = gridDim.x - 2;
+  // block 0: the tail; blocks 1..n_rows: router rows.  The previous step's
+  // deferred update_after_layer ran in arc_update_kernel on the side stream
+  // (overlapping that step's transfers and K3) and completed before this launch.
+  const int n_rows = gridDim.x - 1;
   const int row = blockIdx.x - 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_prof[0] = gtime1();
-  if (blockIdx.x == gridDim.x - 1) {
-    // (1) deferred update_after_layer of the previous step, concurrent with the
-    // router rows (it touches layer l-1's tables and the free stack)
-    if (threadIdx.x < 32 && d.ctrl->prev_valid) apply_prev_update(d, &S.arc, log, S.rel);
-  } else if (blockIdx.x > 0) {
+  if (threadIdx.x == 0 && blockIdx.x == 1) g_k1_prof[10] = gtime1();
+  if (blockIdx.x > 0) {
     // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
     const int lrow = row < E ? layer : layer + 1;
     const int e_row = row < E ? row : row - E;
@@ -231,7 +229,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (blockIdx.x > 0) {
     if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(&d.ctrl->arrive, 1u);
+      const unsigned prev = atomicAdd(&d.ctrl->arrive, 1u);
+      if (prev == gridDim.x - 2) g_k1_prof[11] = gtime1();  // last arrival
     }
     return;
   }
@@ -495,14 +494,19 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (layer == L - 1) C.next_token = token + 1;
     g_k1_prof[6] = gtime1();
     __threadfence();
+    g_k1_prof[7] = gtime1();
   }
 }
 
-// Final deferred update (after the last decode step) and standalone access.
+// Deferred update_after_layer of the step whose K1 just finished (launched on
+// the side stream after every K1, so it overlaps the step's transfers and K3;
+// the next K1 waits for it), and the final flush.  No-op if already applied.
 __global__ void arc_flush_kernel(EngineDev d, fate_step_log *log) {
   __shared__ ArcLayer arc_sm;
   __shared__ int32_t rel[4 * KMAX + 4];
+  if (threadIdx.x == 0) g_k1_prof[8] = gtime1();
   if (d.ctrl->prev_valid) apply_prev_update(d, &arc_sm, log, rel);
+  if (threadIdx.x == 0) g_k1_prof[9] = gtime1();
 }
 
 // Standalone ARC accesses (update_after_layer / arc_access API).  Newly
@@ -663,6 +667,8 @@ struct fate_engine {
   int32_t *pf_shared_I = nullptr;
   cudaStream_t cstream = nullptr, xstream = nullptr, xstream2 = nullptr;  // compute, two copy streams
   cudaEvent_t xlast[2] = {nullptr, nullptr};  // last copy submitted on each copy stream
+  cudaStream_t astream = nullptr;             // side stream: per-step deferred ARC update
+  cudaEvent_t ev_k1 = nullptr, ev_arc = nullptr;
   int max_total_I = 0;
   int prefill_max_tokens = 0;
   // prefill scratch
@@ -728,7 +734,7 @@ int copy_to_buffers(fate_engine *g, const int32_t *loads_dev, int layer, int bit
 static int prefill_preload();
 
 extern "C" int fate_k1_profile(uint64_t *out_host) {
-  if (cudaMemcpyFromSymbol(out_host, g_k1_prof, sizeof(unsigned long long) * 8) != cudaSuccess) {
+  if (cudaMemcpyFromSymbol(out_host, g_k1_prof, sizeof(unsigned long long) * 16) != cudaSuccess) {
     set_error("fate_k1_profile: copy failed");
     return FATE_ECUDA;
   }
@@ -852,6 +858,9 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   FATE_CUDA(cudaStreamCreateWithPriority(&g->xstream, cudaStreamNonBlocking, lo));
   FATE_CUDA(cudaStreamCreateWithPriority(&g->xstream2, cudaStreamNonBlocking, lo));
   for (auto &e : g->xlast) FATE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  FATE_CUDA(cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, hi));
+  FATE_CUDA(cudaEventCreateWithFlags(&g->ev_k1, cudaEventDisableTiming));
+  FATE_CUDA(cudaEventCreateWithFlags(&g->ev_arc, cudaEventDisableTiming));
   // load every kernel the engine launches now: lazy module loading at first
   // launch can deadlock behind a stream parked on a cuStreamWaitValue32 flag
   {
@@ -884,6 +893,12 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   if (g->xstream2) cudaStreamDestroy(g->xstream2);
   for (auto &e : g->xlast)
     if (e) cudaEventDestroy(e);
+  if (g->astream) {
+    cudaStreamSynchronize(g->astream);
+    cudaStreamDestroy(g->astream);
+  }
+  if (g->ev_k1) cudaEventDestroy(g->ev_k1);
+  if (g->ev_arc) cudaEventDestroy(g->ev_arc);
   cudaFree(g->pool);
   cudaFree(g->dev_block);
   if (g->pf_block) cudaFree(g->pf_block);
@@ -1201,12 +1216,20 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     while (launched < n_steps && launched < processed + (serial ? 1 : lookahead) && (!serial || k3_next == launched)) {
       const int s = launched, t = s / L, l = s % L;
       // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
-      const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
+      // tail block + router rows of W_l (and W_{l+1} when predicting)
+      const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 1;
+      FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));  // previous step's ARC update applied
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
       decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
                                                         (volatile uint32_t *)g->ready_dev, t);
       FATE_CHECK_LAUNCH("decode_gate_kernel");
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
+      // update_after_layer of this step (pipeline.py:483) on the side stream
+      FATE_CUDA(cudaEventRecord(g->ev_k1, cs));
+      FATE_CUDA(cudaStreamWaitEvent(g->astream, g->ev_k1, 0));
+      arc_flush_kernel<<<1, 32, 0, g->astream>>>(g->d, log_dev);
+      FATE_CHECK_LAUNCH("arc_flush_kernel (step update)");
+      FATE_CUDA(cudaEventRecord(g->ev_arc, g->astream));
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
       FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
                                   CU_STREAM_WAIT_VALUE_GEQ));
@@ -1306,9 +1329,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     if ((status = ffn_step(k3_next))) break;
     ++k3_next;
   }
+  cudaStreamWaitEvent(cs, g->ev_arc, 0);
   arc_flush_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
   cudaError_t fe = cudaGetLastError();
   cudaError_t se = cudaStreamSynchronize(cs);
+  if (se == cudaSuccess) se = cudaStreamSynchronize(g->astream);
   cudaError_t xe = cudaStreamSynchronize(g->xstream);
   if (xe == cudaSuccess) xe = cudaStreamSynchronize(g->xstream2);
   if (status == FATE_OK && fe != cudaSuccess) status = cuda_status(fe, "arc_flush_kernel");

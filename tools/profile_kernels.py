@@ -235,11 +235,12 @@ def allhit(iters: int):
     st = res.stats
     from paper_2502_12224_b200 import _lib
     print_k3_trace(_lib)
-    k1 = np.zeros(8, dtype=np.uint64)
+    k1 = np.zeros(16, dtype=np.uint64)
     _lib.load().fate_k1_profile(k1.ctypes.data)
     k1 = (k1.astype(np.float64) - float(k1[0])) / 1000.0
-    print("K1 phases (us): tail_start %.2f staged %.2f routed %.2f split %.2f predicted %.2f posted %.2f" %
-          tuple(k1[1:7]))
+    print("K1 (us from tail-block start): row1_start %.2f last_row_arrival %.2f arc_start %.2f arc_end %.2f "
+          "tail_sees_all %.2f staged %.2f routed %.2f split %.2f predicted %.2f posted %.2f tail_end %.2f" %
+          (k1[10], k1[11], k1[8], k1[9], k1[1], k1[2], k1[3], k1[4], k1[5], k1[6], k1[7]))
     print(json.dumps({"tokens": iters, "gpu_ms": st["gpu_ms"], "tok_s": iters / st["gpu_ms"] * 1e3, "wall_s": wall,
                       "k3_ms": st["ffn_ms"] / st["steps"], "k1_ms": st["gate_ms"] / st["steps"],
                       "k3_gbs": st["ffn_bytes"] / st["steps"] / (st["ffn_ms"] / st["steps"] * 1e-3) / 1e9,
