@@ -282,6 +282,14 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   }
   __syncthreads();
   for (int i = threadIdx.x; i < S.c_pred_n; i += kGateThreads) S.pred_prev[i] = C.pred_list[i];
+  // (2) routing of layer l and the cross-layer prediction for l+1: the two
+  // softmaxes on warps 0 and 1 at once, then the ranks by the whole block
+  const bool pred_seg = d.use_predictor && layer + 1 < L;
+  if ((threadIdx.x >> 5) == 0) warp_softmax(S.z, S.w, E);
+  else if ((threadIdx.x >> 5) == 1 && pred_seg) warp_softmax(S.z + E, S.w + E, E);
+  __syncthreads();
+  if (threadIdx.x < kGateThreads / 2) rank_by_weight(S.w, S.ord, E, threadIdx.x, kGateThreads / 2);
+  else if (pred_seg) rank_by_weight(S.w + E, S.ord + E, E, threadIdx.x - kGateThreads / 2, kGateThreads / 2);
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
@@ -290,8 +298,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   const int step = S.c_step;
   fate_step_log *lg = log ? log + step : nullptr;
   if (lane == 0) g_k1_prof[2] = gtime1();
-  // (2) routing of layer l: softmax + rank (gatesim.py:113-123, core.py:159-163)
-  warp_softmax_rank(S.z, S.w, S.ord, E, k, 0, d.q);
+  // (2) routing of layer l (gatesim.py:113-123, core.py:159-163): S.w / S.ord above
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   // chosen ids in ascending order (pipeline.py:441 iterates sorted(chosen)):
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
   int n_pf = 0, n_pred = -1;
   if (d.use_predictor && layer + 1 < L) {
-    const int len = warp_softmax_rank(S.z + E, S.w + E, S.ord + E, E, k, d.policy, d.q);
+    const int len = warp_pred_len(S.w + E, S.ord + E, E, k, d.policy, d.q);  // S.w / S.ord + E above
     n_pred = len < d.budget_n ? len : d.budget_n;
     for (int base = 0; base < n_pred; base += 32) {
       const int i = base + lane;

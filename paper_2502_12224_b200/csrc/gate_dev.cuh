@@ -75,4 +75,53 @@ __device__ inline int warp_softmax_rank(const double *z, double *w, int32_t *ord
   return cnt > top_k ? cnt : (top_k < E ? top_k : E);
 }
 
+// The pieces of warp_softmax_rank, for callers that spread the work: the
+// softmax (same per-lane order and butterfly as above, so w is bit-identical),
+// the rank by (-w, id) over any set of threads (pure comparisons: exact in any
+// order), and the policy's prediction-prefix length from w and order.
+__device__ inline void warp_softmax(const double *z, double *w, int E) {
+  const int lane = threadIdx.x & 31;
+  double mx = -INFINITY;
+  for (int e = lane; e < E; e += 32) mx = fmax(mx, z[e]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double sum = 0.0;
+  for (int e = lane; e < E; e += 32) {
+    const double v = exp(__dsub_rn(z[e], mx));
+    w[e] = v;
+    sum += v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) w[e] = __ddiv_rn(w[e], sum);
+  __syncwarp();
+}
+
+__device__ inline void rank_by_weight(const double *w, int32_t *order, int E, int t0, int nthreads) {
+  for (int e = t0; e < E; e += nthreads) {
+    const double we = w[e];
+    int r = 0;
+#pragma unroll 8
+    for (int j = 0; j < E; ++j) {
+      const double wj = w[j];
+      r += (wj > we) || (wj == we && j < e);
+    }
+    order[r] = e;
+  }
+}
+
+__device__ inline int warp_pred_len(const double *w, const int32_t *order, int E, int top_k, int policy, double q) {
+  const int lane = threadIdx.x & 31;
+  if (policy == 0) return top_k < E ? top_k : E;
+  int rank = (int)ceil(q * (double)E);
+  rank = rank < 1 ? 1 : (rank > E ? E : rank);
+  const double thr = w[order[E - rank]];
+  int cnt = 0;
+  for (int e = lane; e < E; e += 32) cnt += (w[e] > thr);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  return cnt > top_k ? cnt : (top_k < E ? top_k : E);
+}
+
 }  // namespace fate
