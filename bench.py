@@ -236,6 +236,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--peer-fetch", action="store_true",
+                    help="also time the expert-sharded peer-fetch mode (one shared model across ranks)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -260,7 +262,8 @@ def main():
     cfg = qwen_cfg()
     T = args.tokens
     trace, weights = make_trace(cfg, T, seed=rank)
-    store = ExpertStore(cfg, bits=(4, 2), seed=rank, shared_intermediate=QWEN["shared"], shared_bits=16)
+    store = ExpertStore(cfg, bits=(4, 2), seed=0 if args.peer_fetch else rank, shared_intermediate=QWEN["shared"],
+                        shared_bits=16)
     budget = cfg.dense_bytes + QWEN["slots"] * cfg.expert_bytes[4]
     plan = plan_allocation(cfg, budget, 4)
     strategy = P.Strategy.fate()
@@ -366,6 +369,31 @@ def main():
         cpu = {"value": args.cpu_tokens / secs, "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"first {args.cpu_tokens} tokens of the same trace, 24 layers (fp64 gate + top-4 + "
                          "dequant-fused INT4 routed + bf16 shared FFN, C threads over rows)"}
+    # expert-sharded peer-fetch mode (BASELINE configs[4]): each rank
+    # homes (l*E+e) mod G of the experts in its HBM; misses are device/peer copies
+    peer = None
+    if args.peer_fetch:
+        from paper_2502_12224_b200.replicas import ExpertShards
+        shards = ExpertShards(store, bits=(4, 2), rank=rank, world_size=world, device=dev)
+        shards.attach(eng)
+        eng.reset_cache()
+        eng.decode(gd, chd)
+        pst = []
+        for _ in range(2):
+            eng.reset_cache()
+            pst.append(eng.decode(gd, chd).stats)
+        p_s = sum(x["gpu_ms"] for x in pst) / 1000.0
+        if world > 1:
+            tt = torch.tensor([p_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            p_s = float(tt.item())
+        peer = {"workload": f"Qwen1.5-MoE shape decode, experts sharded over {world} GPU(s), misses served "
+                            "from the home GPU's HBM (NVLink peer copy for remote homes)",
+                "tokens_per_s": T * len(pst) * world / p_s, "home_pool_bytes_per_gpu": shards.device_bytes,
+                "d2d_bytes": sum(x["d2d_bytes"] for x in pst), "h2d_bytes": sum(x["h2d_bytes"] for x in pst),
+                "k3_ms_per_launch": sum(x["ffn_ms"] for x in pst) / sum(x["steps"] for x in pst)}
+        shards.detach(eng)
+        shards.close()
     pre = None
     if not args.no_prefill:
         eng.close()
@@ -404,6 +432,7 @@ def main():
             "k1_ms_per_launch": agg["gate_ms"] / agg["steps"],
             "trace_mismatches": agg["trace_mismatches"],
             "prefill": pre,
+            "peer_fetch": peer,
             "wall_s_timed": wall,
         }
         print(json.dumps(out), flush=True)

@@ -173,6 +173,20 @@ int fate_engine_set_gate(fate_engine *eng, const double *W_host, const double *t
 /* Register the pinned host pool for one bit width: experts (l,e) at
  * base + (l*E + e) * stride, each a packed buffer (header + payload). */
 int fate_engine_set_host_pool(fate_engine *eng, int bits, const uint8_t *base_host, int64_t stride);
+/* Expert-sharded peer-fetch mode: per-expert source buffers for
+ * one bit width, srcs[l*E + e] = a packed buffer (header + payload) in device
+ * memory of this GPU or of a peer GPU mapped into this process (CUDA IPC,
+ * fate_ipc_open_handle), or NULL to keep the pinned host copy.  A miss of
+ * (l, e) at that width is then a device/peer copy (cudaMemcpyDefault: NVLink
+ * for peers) instead of a host fetch; decisions are unchanged.  srcs == NULL
+ * clears the table.  The array is copied. */
+int fate_engine_set_expert_sources(fate_engine *eng, int bits, const uint8_t *const *srcs);
+/* CUDA IPC for the home shards of the expert-sharded mode: export the device
+ * allocation containing dev_ptr (64-byte handle + dev_ptr's byte offset in it),
+ * map a peer's allocation (add the offset to the returned base), unmap it. */
+int fate_ipc_get_handle(const void *dev_ptr, uint8_t *handle64, int64_t *offset);
+int fate_ipc_open_handle(const uint8_t *handle64, void **dev_ptr_out);
+int fate_ipc_close(void *dev_ptr);
 /* Shared expert for layer l: a packed device buffer (resident, dense bytes). */
 int fate_engine_set_shared(fate_engine *eng, int layer, const uint8_t *buf_dev);
 
@@ -221,6 +235,8 @@ typedef struct fate_run_stats {
   int64_t ffn_bytes;          /* algorithmic bytes of executed experts     */
   double ffn_flops;           /* prefill: 2*3*H*I*tokens summed            */
   int64_t near_ties;          /* k-th/(k+1)-th weight gap < 1e-12           */
+  int64_t d2d_bytes;          /* misses served from device memory (local or
+                                 peer HBM over NVLink, expert-sharded mode)    */
   int32_t error; int32_t pad;
 } fate_run_stats;
 

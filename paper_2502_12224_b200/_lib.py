@@ -62,7 +62,8 @@ class RunStats(C.Structure):
         ("dequant_count", c_i64), ("prefetch_issued", c_i64), ("ondemand_issued", c_i64),
         ("transfers_done", c_i64), ("transfers_dropped", c_i64), ("h2d_bytes", c_i64),
         ("copy_busy_ms", c_dbl), ("recall_sum", c_dbl), ("recall_n", c_i64), ("trace_mismatches", c_i64),
-        ("ffn_bytes", c_i64), ("ffn_flops", c_dbl), ("near_ties", c_i64), ("error", C.c_int32), ("pad", C.c_int32),
+        ("ffn_bytes", c_i64), ("ffn_flops", c_dbl), ("near_ties", c_i64), ("d2d_bytes", c_i64),
+        ("error", C.c_int32), ("pad", C.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -83,6 +84,10 @@ SIGNATURES = {
     "fate_gate_forward": (c_int, [c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp]),
     "fate_ffn_decode": (c_int, [c_vp, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_vp, c_vp]),
     "fate_k3_profile": (c_int, [c_vp]),
+    "fate_engine_set_expert_sources": (c_int, [c_vp, c_int, c_vp]),
+    "fate_ipc_get_handle": (c_int, [c_vp, c_vp, C.POINTER(c_i64)]),
+    "fate_ipc_open_handle": (c_int, [c_vp, C.POINTER(c_vp)]),
+    "fate_ipc_close": (c_int, [c_vp]),
     "fate_ffn_decode_timed": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_int,
                                       c_vp, C.POINTER(C.c_float)]),
     "fate_k1_profile": (c_int, [c_vp]),

@@ -668,6 +668,7 @@ struct fate_engine {
   CUdeviceptr copy_done_dev = 0, copy_done_dev2 = 0;
   // host pools
   const uint8_t *host_pool[17] = {};
+  std::vector<const uint8_t *> src_table[17];  // expert-sharded mode: per-(l,e) device/peer sources
   int64_t host_stride[17] = {};
   std::vector<const uint8_t *> shared_dev;
   const uint8_t **shared_table_dev = nullptr;
@@ -933,6 +934,60 @@ extern "C" int fate_engine_set_host_pool(fate_engine *g, int bits, const uint8_t
   return FATE_OK;
 }
 
+extern "C" int fate_engine_set_expert_sources(fate_engine *g, int bits, const uint8_t *const *srcs) {
+  if (!(bits == 2 || bits == 4 || bits == 8 || bits == 16)) {
+    set_error("fate_engine_set_expert_sources: bits must be 2, 4, 8 or 16");
+    return FATE_EINVAL;
+  }
+  auto &t = g->src_table[bits];
+  if (!srcs) {
+    t.clear();
+    return FATE_OK;
+  }
+  const size_t n = (size_t)g->cfg.num_layers * g->cfg.num_experts;
+  t.assign(srcs, srcs + n);
+  return FATE_OK;
+}
+
+typedef CUresult (*PFN_addr_range)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+// IPC handles name whole allocations: export the allocation that contains
+// dev_ptr (a caching allocator may sub-allocate) and return dev_ptr's offset.
+extern "C" int fate_ipc_get_handle(const void *dev_ptr, uint8_t *handle64, int64_t *offset) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  static PFN_addr_range p_range = nullptr;
+  if (!p_range) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f) {
+      set_error("fate_ipc_get_handle: cuMemGetAddressRange unavailable");
+      return FATE_ECUDA;
+    }
+    p_range = (PFN_addr_range)f;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  FATE_CU(p_range(&base, &size, (CUdeviceptr)dev_ptr));
+  cudaIpcMemHandle_t h;
+  FATE_CUDA(cudaIpcGetMemHandle(&h, (void *)base));
+  memcpy(handle64, &h, 64);
+  *offset = (int64_t)((CUdeviceptr)dev_ptr - base);
+  return FATE_OK;
+}
+
+extern "C" int fate_ipc_open_handle(const uint8_t *handle64, void **dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  FATE_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return FATE_OK;
+}
+
+extern "C" int fate_ipc_close(void *dev_ptr) {
+  FATE_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return FATE_OK;
+}
+
 extern "C" int fate_engine_set_shared(fate_engine *g, int layer, const uint8_t *buf_dev) {
   if (layer < 0 || layer >= g->cfg.num_layers || !g->cfg.shared_intermediate) {
     set_error("fate_engine_set_shared: bad layer or engine has no shared expert");
@@ -1026,7 +1081,7 @@ struct Channel {
   std::deque<Transfer> pending;
   std::deque<Inflight> inflight;
   uint32_t submitted = 0;
-  int64_t h2d_bytes = 0, done = 0, dropped = 0;
+  int64_t h2d_bytes = 0, d2d_bytes = 0, done = 0, dropped = 0;
   bool timed = false;
   cudaEvent_t t0 = nullptr;      // run start, for absolute copy timestamps
   std::vector<cudaEvent_t> ev;  // pairs, recycled through ev_free once reaped
@@ -1054,19 +1109,23 @@ struct Channel {
         return FATE_EINVAL;
       }
       const int64_t bytes = bytes_of(t.bits);
-      const uint8_t *src = g->host_pool[t.bits] + ((int64_t)t.layer * g->cfg.num_experts + t.expert) * g->host_stride[t.bits];
+      const int64_t le = (int64_t)t.layer * g->cfg.num_experts + t.expert;
+      const auto &tab = g->src_table[t.bits];
+      const uint8_t *dsrc = tab.empty() ? nullptr : tab[le];  // expert-sharded mode: device / peer copy
+      const uint8_t *src = dsrc ? dsrc : g->host_pool[t.bits] + le * g->host_stride[t.bits];
       if (timed && !ev_free.empty()) {
         evi = ev_free.back();
         ev_free.pop_back();
         FATE_CUDA(cudaEventRecord(ev[evi], s));
       }
-      FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)t.buf * g->buf_stride, src, bytes, cudaMemcpyHostToDevice, s));
+      FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)t.buf * g->buf_stride, src, bytes,
+                                dsrc ? cudaMemcpyDefault : cudaMemcpyHostToDevice, s));
       if (evi >= 0) FATE_CUDA(cudaEventRecord(ev[evi + 1], s));
       // landed marks are read only for queued prefetches (K1's arrival check):
       // on-demand copies skip the extra stream op between back-to-back copies
       if (t.kind == 0) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
       FATE_CUDA(cudaEventRecord(g->xlast[si], s));
-      h2d_bytes += bytes;
+      (dsrc ? d2d_bytes : h2d_bytes) += bytes;
     }
     // the step's wait flag is released by the copy streams themselves right
     // after the last transfer the step needs (the host also sets it when reaping)
@@ -1387,6 +1446,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   st.transfers_done = ch.done;
   st.transfers_dropped = ch.dropped;
   st.h2d_bytes = ch.h2d_bytes;
+  st.d2d_bytes = ch.d2d_bytes;
   st.copy_busy_ms = ch.copy_ms;
   st.recall_sum = ds.recall_sum;
   st.recall_n = (int64_t)ds.recall_n;
@@ -2101,6 +2161,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   st.transfers_done = ch.done;
   st.transfers_dropped = ch.dropped;
   st.h2d_bytes = ch.h2d_bytes;
+  st.d2d_bytes = ch.d2d_bytes;
   st.copy_busy_ms = ch.copy_ms;
   st.recall_sum = ds.recall_sum;
   st.recall_n = (int64_t)ds.recall_n;

@@ -121,6 +121,18 @@ class OffloadEngine:
                                          hits.ctypes.data_as(C.POINTER(C.c_int32))), "fate_engine_access")
         return [bool(h) for h in hits]
 
+    def set_expert_sources(self, bits: int, ptrs) -> None:
+        """Expert-sharded mode: misses of width ``bits`` copy from ptrs[l*E + e]
+        (device or peer buffers; 0 keeps the host copy).  ``None`` clears."""
+        if ptrs is None:
+            check(self._L.fate_engine_set_expert_sources(self._h, bits, None), "fate_engine_set_expert_sources")
+            return
+        n = self.cfg.num_layers * self.cfg.num_experts
+        if len(ptrs) != n:
+            raise InvalidConfig(f"expected {n} source pointers, got {len(ptrs)}")
+        arr = (C.c_void_p * n)(*[int(p) or None for p in ptrs])
+        check(self._L.fate_engine_set_expert_sources(self._h, bits, arr), "fate_engine_set_expert_sources")
+
     def seed_resident(self, layer: int, experts) -> None:
         ex = np.ascontiguousarray(np.asarray(list(experts), dtype=np.int32))
         check(self._L.fate_engine_seed_resident(self._h, layer, ex.ctypes.data_as(C.POINTER(C.c_int32)), len(ex)),

@@ -61,3 +61,25 @@ def test_two_rank_replicas_gloo():
     assert n0 + n1 == 32 and n0 == 16                 # expert homes partition (l*E+e) mod G
     from paper_2502_12224_b200 import replicas
     assert replicas.home_rank(1, 3, 8, 2) == 1
+
+
+@pytest.mark.parametrize("L,E,G", [(24, 60, 1), (24, 60, 2), (28, 64, 8), (4, 8, 3)])
+def test_shard_layout_partitions_and_addresses(L, E, G):
+    # expert-sharded peer-fetch mode: every expert has exactly one home slot,
+    # homes are balanced, and source addresses never collide
+    from paper_2502_12224_b200.replicas import home_rank, shard_layout, source_table
+    homes, slot = shard_layout(L, E, G)
+    assert sorted(le for h in homes for le in h) == [(l, e) for l in range(L) for e in range(E)]
+    sizes = [len(h) for h in homes]
+    assert max(sizes) - min(sizes) <= 1
+    for r, h in enumerate(homes):
+        assert all(home_rank(l, e, E, G) == r for (l, e) in h)
+        assert [slot[le] for le in h] == list(range(len(h)))
+    stride = 4096
+    bases = [(r + 1) << 40 for r in range(G)]
+    tab = source_table(L, E, G, bases, stride)
+    assert len(tab) == L * E and len(set(tab)) == L * E
+    for l in range(L):
+        for e in range(E):
+            r = home_rank(l, e, E, G)
+            assert tab[l * E + e] == bases[r] + slot[(l, e)] * stride
