@@ -395,7 +395,9 @@ def main():
         shards.detach(eng)
         shards.close()
     pre = None
-    if not args.no_prefill:
+    # prefill (configs[2]) is a single-GPU workload; under torchrun every rank would
+    # pin its own 15 GB DeepSeek host pools, so it is measured at N = 1 only
+    if not args.no_prefill and world == 1:
         eng.close()
         eng = None
         torch.cuda.empty_cache()

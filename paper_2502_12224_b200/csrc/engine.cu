@@ -461,11 +461,11 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   FfnBatch &B = *d.batch;
   if (act)
     B.e[lane] = FfnExpert{d.pool + (int64_t)b * d.buf_stride, (float)S.w[ce], d.I, hit ? S.bbits_l[ce] : src,
-                          lane * d.I};
+                          lane * d.I, 0};
   if (lane == 0) {
     int n = k, off = k * d.I;
     if (S.shared_present) {
-      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, d.shared_bits, off};
+      B.e[n] = FfnExpert{d.shared_k3[layer], 1.0f, d.I_shared, d.shared_bits, off, d.shared_layout};
       off += d.I_shared;
       ++n;
     }
@@ -672,6 +672,8 @@ struct fate_engine {
   int64_t host_stride[17] = {};
   std::vector<const uint8_t *> shared_dev;
   const uint8_t **shared_table_dev = nullptr;
+  std::vector<uint8_t *> shared_k3;            // owned K3 copies (bf16: W2 slab-major)
+  const uint8_t **shared_k3_table_dev = nullptr;
   int32_t *pf_shared_I = nullptr;
   cudaStream_t cstream = nullptr, xstream = nullptr, xstream2 = nullptr;  // compute, two copy streams
   cudaEvent_t xlast[2] = {nullptr, nullptr};  // last copy submitted on each copy stream
@@ -814,7 +816,7 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
                o_bb = carve((size_t)nbuf * 4),
                o_ctrl = carve(sizeof(Ctrl)), o_st = carve(sizeof(DevStats)), o_lg = carve(2 * EMAX * 8),
                o_x = carve(ffn_xlay_floats(H) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
-               o_sh = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
+               o_sh = carve((size_t)L * 8), o_sh3 = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
                o_a = carve(ffn_alay_floats(g->max_total_I) * 4);
   FATE_CUDA(cudaMalloc(&g->dev_block, off));
   FATE_CUDA(cudaMemset(g->dev_block, 0, off));
@@ -837,12 +839,16 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   g->caps_dev = (int32_t *)(base + o_caps);
   g->shared_table_dev = (const uint8_t **)(base + o_sh);
   d.shared = cfg->shared_intermediate ? g->shared_table_dev : nullptr;
+  g->shared_k3_table_dev = (const uint8_t **)(base + o_sh3);
+  d.shared_k3 = g->shared_k3_table_dev;
+  d.shared_layout = cfg->shared_bits == 16 ? 1 : 0;
   g->scratch_i = (int32_t *)(base + o_si);
   g->a_scratch = (float *)(base + o_a);
   FATE_CUDA(cudaMalloc(&g->pool, (size_t)nbuf * g->buf_stride));
   d.pool = g->pool;
   FATE_CUDA(cudaMemcpy(g->caps_dev, g->caps.data(), L * 4, cudaMemcpyHostToDevice));
   g->shared_dev.assign(L, nullptr);
+  g->shared_k3.assign(L, nullptr);
   // mapped pinned host memory: mailbox ring, ready flags, copy counter
   void *p = nullptr;
   FATE_CUDA(cudaHostAlloc(&p, sizeof(StepMsg) * kRing, cudaHostAllocMapped));
@@ -909,6 +915,8 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   if (g->ev_arc) cudaEventDestroy(g->ev_arc);
   cudaFree(g->pool);
   cudaFree(g->dev_block);
+  for (auto *p : g->shared_k3)
+    if (p) cudaFree(p);
   if (g->pf_block) cudaFree(g->pf_block);
   cudaFreeHost(g->ring_host);
   cudaFreeHost((void *)g->ready_host);
@@ -932,6 +940,17 @@ extern "C" int fate_engine_set_host_pool(fate_engine *g, int bits, const uint8_t
   g->host_pool[bits] = base;
   g->host_stride[bits] = stride;
   return FATE_OK;
+}
+
+// W2 [H, I] row-major -> column slabs: slab t = columns [t*kSlabCols, t*kSlabCols + w_t)
+// of all H rows, row-major inside (w_t = kSlabCols, the last one narrower).
+__global__ void slab_w2_kernel(const __nv_bfloat16 *__restrict__ w2, int H, int I, __nv_bfloat16 *__restrict__ out) {
+  const int64_t n = (int64_t)H * I;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int h = (int)(i / I), c = (int)(i % I);
+    const int k0 = c / kSlabCols * kSlabCols, w = min(kSlabCols, I - k0);
+    out[(int64_t)H * k0 + (int64_t)h * w + (c - k0)] = w2[i];
+  }
 }
 
 extern "C" int fate_engine_set_expert_sources(fate_engine *g, int bits, const uint8_t *const *srcs) {
@@ -996,6 +1015,22 @@ extern "C" int fate_engine_set_shared(fate_engine *g, int layer, const uint8_t *
   g->shared_dev[layer] = buf_dev;
   FATE_CUDA(cudaMemcpy(g->shared_table_dev, g->shared_dev.data(), g->cfg.num_layers * sizeof(void *),
                        cudaMemcpyHostToDevice));
+  // K3's own copy: bf16 W2 re-laid into column slabs (one bulk copy per phase-B tile)
+  const int H = g->cfg.hidden_dim, Is = g->cfg.shared_intermediate, bits = g->cfg.shared_bits;
+  const int64_t bytes = buffer_bytes(H, Is, bits);
+  if (!g->shared_k3[layer]) FATE_CUDA(cudaMalloc(&g->shared_k3[layer], bytes));
+  uint8_t *dst = g->shared_k3[layer];
+  FATE_CUDA(cudaMemcpy(dst, buf_dev, bytes, cudaMemcpyDeviceToDevice));
+  if (bits == 16) {
+    const Layout Lo = make_layout(H, Is, 16);
+    const __nv_bfloat16 *w2 = reinterpret_cast<const __nv_bfloat16 *>(buf_dev + FATE_HEADER_BYTES + Lo.c2);
+    __nv_bfloat16 *o2 = reinterpret_cast<__nv_bfloat16 *>(dst + FATE_HEADER_BYTES + Lo.c2);
+    slab_w2_kernel<<<148 * 4, 256, 0, g->cstream>>>(w2, H, Is, o2);
+    FATE_CHECK_LAUNCH("slab_w2_kernel");
+    FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  }
+  std::vector<const uint8_t *> t(g->shared_k3.begin(), g->shared_k3.end());
+  FATE_CUDA(cudaMemcpy(g->shared_k3_table_dev, t.data(), g->cfg.num_layers * sizeof(void *), cudaMemcpyHostToDevice));
   return FATE_OK;
 }
 

@@ -97,7 +97,14 @@ struct FfnExpert {
   int I;
   int bits;
   int a_off;           // offset of this expert's activation vector in scratch
+  int layout;          // 0: row-major; 1: bf16 W2 stored in column slabs of kSlabCols (K3-only copy)
 };
+
+// Column-slab width of the K3-only copy of a resident bf16 expert's W2
+// (= K3's phase-B K-range for bf16: 96 chunks x 8 columns): slab t holds
+// columns [t*kSlabCols, ...) of all H rows contiguously, so any phase-B tile
+// (consecutive rows of one K-range) is a single bulk copy.
+constexpr int kSlabCols = 768;
 
 constexpr int kMaxFfnExperts = FATE_MAX_TOPK + 2;
 

@@ -576,21 +576,37 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       if (++stage == stages) stage = 0, phase ^= 1;
       return end;
     };
-    // static round-robin over the tile list (expert-major, so every CTA gets
-    // a proportional mix of each expert's format); then the end marker
-    for (int t = blockIdx.x;; t += gridDim.x)
-      if (step_a(t)) break;
+    // static round-robin over the tile list (expert-major, so every CTA gets a
+    // proportional mix of each expert's format), walked alternately from both
+    // ends so compute-heavy quantized tiles interleave with bf16 streaming
+    // tiles; then the end marker
+    {
+      const int K = plan.n_a > (int)blockIdx.x ? (plan.n_a - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+      for (int i = 0; i < K; ++i) {
+        const int kk = (i & 1) ? K - 1 - (i >> 1) : (i >> 1);
+        step_a((int)blockIdx.x + kk * (int)gridDim.x);
+      }
+      step_a(plan.n_a);  // end marker
+    }
     for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x) {
       const int R0 = blk * plan.RBB, rows = min(plan.RBB, H - R0);
       for (int s0 = 0; s0 < rows; s0 += kSubRows) {
         const int nr = min(kSubRows, rows - s0), rs0 = R0 + s0;
-        for (int j = 0; j < batch.n; ++j) {
+        // the sub-block's tiles (expert j, K-range kt), walked alternately from
+        // both ends of the expert-major list (routed quantized tiles interleave
+        // with the shared expert's bf16 tiles); the last one carries the flush
+        int total = 0;
+        for (int j = 0; j < batch.n; ++j) total += plan.ktiles[j];
+        for (int i = 0; i < total; ++i) {
+          int pos = (i & 1) ? total - 1 - (i >> 1) : (i >> 1), j = 0;
+          while (pos >= plan.ktiles[j]) pos -= plan.ktiles[j], ++j;
+          const int kt = pos;
           const FfnExpert &ex = batch.e[j];
           const int bits = ex.bits;
           const Layout L = make_layout(H, ex.I, bits);
           const int64_t rb = L.row_bytes_down, szb = sz_row_bytes(ex.I, bits);
           const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
-          for (int kt = 0; kt < plan.ktiles[j]; ++kt) {
+          {
             const int k0 = kt * plan.colsB[j], nc = min(plan.colsB[j], ex.I - k0);
             const uint32_t cb = (uint32_t)nc * bits / 8, sb = bits == 16 ? 0u : (uint32_t)nc / 8;
             K3_TRACE(0, ti, 0);
@@ -604,11 +620,15 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
               m.nr = nr;
               m.k0 = k0;
               m.nc = nc;
-              m.flush = (j == batch.n - 1 && kt == plan.ktiles[j] - 1);
+              m.flush = i == total - 1;
               mbar_expect_tx(&ring.full[stage], (uint32_t)nr * (cb + sb));
             }
             __syncwarp();
-            if (nc == ex.I) {
+            if (ex.layout == 1) {
+              // bf16 W2 in column slabs (kSlabCols == this K-range): the tile's rows are contiguous
+              if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)H * k0 * 2 + (int64_t)rs0 * nc * 2,
+                                      nr * cb, &ring.full[stage]);
+            } else if (nc == ex.I) {
               // whole rows: the tile's rows are contiguous in the buffer, one copy
               // for the codes and one for the (scale, zero) pairs
               if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)rs0 * rb, nr * cb, &ring.full[stage]);
@@ -867,7 +887,7 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
       set_error("fate_ffn_decode: buffer header does not describe a packed expert of this hidden size");
       return FATE_EINVAL;
     }
-    b.e[j] = FfnExpert{bufs[j], weights[j], h.I, h.bits, off};
+    b.e[j] = FfnExpert{bufs[j], weights[j], h.I, h.bits, off, 0};
     off += h.I;
   }
   b.total_I = off;
@@ -912,7 +932,7 @@ extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets
         set_error("fate_ffn_decode_timed: buffer header does not describe a packed expert of this hidden size");
         return FATE_EINVAL;
       }
-      b.e[j] = FfnExpert{buf, weights[j], h.I, h.bits, off};
+      b.e[j] = FfnExpert{buf, weights[j], h.I, h.bits, off, 0};
       off += h.I;
     }
     b.total_I = off;

@@ -215,6 +215,43 @@ def timeline(tokens: int):
                       "step_us_mean": float((sm[-1][3] - sm[0][0]) / n * 1e3)}))
 
 
+def mixtral(tokens: int):
+    """BASELINE configs[3]: Mixtral-8x7B shape (32 layers, 8 experts top-2, H 4096,
+    I 14336), decode with quantized prefetch (Strategy.fate()), budget sweep
+    S in {0, 32, 64, 128, 192, 256} INT4 slots (0-100% of 256), cold cache."""
+    from paper_2502_12224_b200 import pipeline as P
+    from paper_2502_12224_b200.cache import plan_allocation
+    from paper_2502_12224_b200.core import ModelConfig
+    from paper_2502_12224_b200.engine import OffloadEngine
+    from paper_2502_12224_b200.experts import ExpertStore
+    from paper_2502_12224_b200.gatesim import GenConfig, gen_trace
+    cfg = ModelConfig.from_shape(32, 8, 2, 4096, 14336, 1, dense_bytes=0)
+    tr, w = gen_trace(cfg, GenConfig(seed=0, num_tokens=tokens, phase="decoding"))
+    store = ExpertStore(cfg, bits=(4, 2), seed=0)
+    _, g, ch = tr.dense_arrays(cfg)
+    gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
+    strategy = P.Strategy.fate()
+    rows = []
+    for S in (0, 32, 64, 128, 192, 256):
+        plan = plan_allocation(cfg, cfg.dense_bytes + S * cfg.expert_bytes[4], 4)
+        # n = 2: the whole percentile-0.75 prediction at E = 8 (= top-2) is prefetched
+        eng = OffloadEngine(cfg, plan.per_layer_capacity, store, w, P.knobs_for(strategy, plan, 2),
+                            max_tokens=max(tokens, 64))
+        eng.decode(gd[:4], chd[:4])
+        eng.reset_cache()
+        res = eng.decode(gd, chd)
+        st = res.stats
+        rows.append({"slots": S, "plan": list(plan.per_layer_capacity)[:4], "tok_s": tokens / st["gpu_ms"] * 1e3,
+                     "hit_rate_cache": st["cache_hits"] / st["accesses"],
+                     "hit_rate_combined": (st["cache_hits"] + st["arrival_hits"]) / st["accesses"],
+                     "h2d_gb": st["h2d_bytes"] / 1e9, "k3_ms": st["ffn_ms"] / st["steps"],
+                     "k3_gbs": st["ffn_bytes"] / st["steps"] / (st["ffn_ms"] / st["steps"] * 1e-3) / 1e9})
+        eng.close()
+        print(json.dumps(rows[-1]), flush=True)
+    print(json.dumps({"workload": "Mixtral-8x7B shape decode, budget sweep (BASELINE configs[3])", "tokens": tokens,
+                      "rows": rows}))
+
+
 def allhit(iters: int):
     from paper_2502_12224_b200.core import ModelConfig
     from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
@@ -250,4 +287,5 @@ def allhit(iters: int):
 if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline}[mode](it)
+    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline,
+     "mixtral": mixtral}[mode](it)
