@@ -147,8 +147,19 @@ def run_reference(args):
             b[256:].view(np.uint16)[:] = 0x3C00
         return b
 
-    get_buf = lambda l, e: bufs.setdefault((l, e), rand_buf(nb4, I, 4))  # noqa: E731
-    shared = lambda l: bufs.setdefault(("s", l), rand_buf(nb16, Is, 16))  # noqa: E731
+    # every expert buffer the sample touches is built before the timed steps
+    # (setdefault would evaluate rand_buf on every access and time buffer generation)
+    _, g_s, _ = trace.dense_arrays(cfg)
+    for t in range(tokens):
+        for l in range(cfg.num_layers):
+            w_ = O.gate_routing(weights.matrices[l], weights.temperatures[l], g_s[t, l])
+            for e in O.top_k(w_, cfg.top_k):
+                if (l, e) not in bufs:
+                    bufs[(l, e)] = rand_buf(nb4, I, 4)
+    for l in range(cfg.num_layers):
+        bufs[("s", l)] = rand_buf(nb16, Is, 16)
+    get_buf = lambda l, e: bufs[(l, e)]  # noqa: E731
+    shared = lambda l: bufs[("s", l)]  # noqa: E731
     for _ in range(args.warmup):
         cpu_decode(cfg, trace, weights, get_buf, shared, tokens, lib)
     times = [cpu_decode(cfg, trace, weights, get_buf, shared, tokens, lib) for _ in range(args.steps)]

@@ -14,7 +14,8 @@ the reference's (tests/test_gpu_engine.py).
 Extra keyword arguments (not in the reference): ``experts`` (an ExpertStore;
 default: synthetic random-init experts for ``cfg``), ``shared_intermediate``
 (shared expert width for the default store) and ``return_result`` (also
-return the raw engine result with expert outputs and per-step logs).
+return the raw engine result with the expert outputs; ``return_result="logs"``
+adds the per-step device logs, which cost a D2H copy and host parsing).
 """
 
 from __future__ import annotations
@@ -247,7 +248,7 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     cache, eng = bind_engine(cache, plan, cfg, weights, experts, knobs, max_tokens=max(len(toks), 1))
     dev = torch.device("cuda", eng.device)
     res = eng.decode(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev), tokens=toks,
-                     want_logs=collect_cache_events or return_result)
+                     want_logs=collect_cache_events or return_result == "logs")
     st = res.stats
     L = cfg.num_layers
     events = []
