@@ -881,6 +881,10 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
     cudaFuncAttributes fa;
     FATE_CUDA(cudaFuncGetAttributes(&fa, decode_gate_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_flush_kernel));
+    // every kernel of the decode step prefers the max shared-memory carveout
+    // (K3's 205 KB), so SMs do not reconfigure L1/shared between K1 and K3
+    FATE_CUDA(cudaFuncSetAttribute(decode_gate_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    FATE_CUDA(cudaFuncSetAttribute(arc_flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_access_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_seed_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, run_begin_kernel));

@@ -809,6 +809,9 @@ cudaError_t ffn_preload() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  for (const void *f : {(const void *)ffn_kernel<0>, (const void *)ffn_kernel<2048>, (const void *)ffn_kernel<4096>,
+                        (const void *)build_xlay_kernel})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   return e;
 }
 

@@ -35,7 +35,6 @@ constexpr int kEpiWarps = 4, kLoadWarps = 8;
 constexpr int kTcThreads = 32 * (kEpiWarps + kLoadWarps + 1);
 constexpr int kMmaWarp = kEpiWarps + kLoadWarps;
 constexpr int kUpStages = 4, kDnStages = 6;  // bf16 operand ring (UMMA layout)
-constexpr int kLook = 2;                      // raw (packed) stages in flight ahead of the dequant
 constexpr int kTileBytes = BM * BK * 2;  // one 128 x 64 bf16 operand tile (16 KB)
 constexpr int kMaxPrefillExperts = FATE_MAX_EXPERTS + 1;  // routed + shared
 
@@ -219,6 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  const int32_t *__restrict__ tok_idx, const int32_t *__restrict__ zrow, const int *__restrict__ a_off,
                  __nv_bfloat16 *__restrict__ A, float *__restrict__ Z) {
   constexpr int S = UP ? kUpStages : kDnStages;
+  constexpr int kLook = S - 2;  // cp.async stages in flight ahead of the dequant (slot reuse waits on the MMA two stages back)
   constexpr int kStage = UP ? 3 * kTileBytes : 2 * kTileBytes;  // [W1 | W3 | X] or [W2 | A]
   constexpr uint32_t kAccCols = UP ? 256 : 128;                 // per accumulator buffer
   extern __shared__ __align__(1024) uint8_t smem[];  // S operand stages
