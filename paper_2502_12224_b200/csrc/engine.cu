@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
 // Deferred update_after_layer of the step whose K1 just finished (launched on
 // the side stream after every K1, so it overlaps the step's transfers and K3;
 // the next K1 waits for it), and the final flush.  No-op if already applied.
-__global__ void arc_flush_kernel(EngineDev d, fate_step_log *log) {
+__global__ void arc_update_kernel(EngineDev d, fate_step_log *log) {
   __shared__ ArcLayer arc_sm;
   __shared__ int32_t rel[4 * KMAX + 4];
   if (threadIdx.x == 0) g_k1_prof[8] = gtime1();
@@ -880,11 +880,11 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   {
     cudaFuncAttributes fa;
     FATE_CUDA(cudaFuncGetAttributes(&fa, decode_gate_kernel));
-    FATE_CUDA(cudaFuncGetAttributes(&fa, arc_flush_kernel));
+    FATE_CUDA(cudaFuncGetAttributes(&fa, arc_update_kernel));
     // every kernel of the decode step prefers the max shared-memory carveout
     // (K3's 205 KB), so SMs do not reconfigure L1/shared between K1 and K3
     FATE_CUDA(cudaFuncSetAttribute(decode_gate_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    FATE_CUDA(cudaFuncSetAttribute(arc_flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    FATE_CUDA(cudaFuncSetAttribute(arc_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_access_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, arc_seed_kernel));
     FATE_CUDA(cudaFuncGetAttributes(&fa, run_begin_kernel));
@@ -1279,7 +1279,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     const int t = s / L, l = s % L;
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
     FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                       g->max_total_I, &g->d.stats->ffn_bytes, 0, cs));
+                                       g->max_total_I, &g->d.stats->ffn_bytes, cs));
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
     return FATE_OK;
   };
@@ -1332,8 +1332,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       // update_after_layer of this step (pipeline.py:483) on the side stream
       FATE_CUDA(cudaEventRecord(g->ev_k1, cs));
       FATE_CUDA(cudaStreamWaitEvent(g->astream, g->ev_k1, 0));
-      arc_flush_kernel<<<1, 32, 0, g->astream>>>(g->d, log_dev);
-      FATE_CHECK_LAUNCH("arc_flush_kernel (step update)");
+      arc_update_kernel<<<1, 32, 0, g->astream>>>(g->d, log_dev);
+      FATE_CHECK_LAUNCH("arc_update_kernel (step update)");
       FATE_CUDA(cudaEventRecord(g->ev_arc, g->astream));
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
       FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
@@ -1435,13 +1435,13 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     ++k3_next;
   }
   cudaStreamWaitEvent(cs, g->ev_arc, 0);
-  arc_flush_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
+  arc_update_kernel<<<1, 32, 0, cs>>>(g->d, log_dev);
   cudaError_t fe = cudaGetLastError();
   cudaError_t se = cudaStreamSynchronize(cs);
   if (se == cudaSuccess) se = cudaStreamSynchronize(g->astream);
   cudaError_t xe = cudaStreamSynchronize(g->xstream);
   if (xe == cudaSuccess) xe = cudaStreamSynchronize(g->xstream2);
-  if (status == FATE_OK && fe != cudaSuccess) status = cuda_status(fe, "arc_flush_kernel");
+  if (status == FATE_OK && fe != cudaSuccess) status = cuda_status(fe, "arc_update_kernel");
   if (status == FATE_OK && se != cudaSuccess) status = cuda_status(se, "decode compute stream");
   if (status == FATE_OK && xe != cudaSuccess) status = cuda_status(xe, "decode copy stream");
   DevStats ds{};

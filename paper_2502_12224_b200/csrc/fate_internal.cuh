@@ -122,10 +122,8 @@ static_assert(sizeof(FfnBatch) % 16 == 0, "K3 copies the batch with 16-byte load
 // scratch (ffn_alay_floats(max_total_I) floats).  The batch is in DEVICE memory.
 cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
                               int max_total_I, cudaStream_t s);
-// accumulate = 1: y += result (the routed launch after the shared-expert launch of the same step)
 cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev,
-                                     int H, int max_total_I, unsigned long long *bytes_stat, int accumulate,
-                                     cudaStream_t s);
+                                     int H, int max_total_I, unsigned long long *bytes_stat, cudaStream_t s);
 cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s);
 size_t ffn_xlay_floats(int H);
 size_t ffn_alay_floats(int max_total_I);

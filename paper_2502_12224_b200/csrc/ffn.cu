@@ -478,7 +478,7 @@ template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
                                                           const float4 *__restrict__ xlay, float *__restrict__ alay,
                                                           float *__restrict__ y, unsigned long long *bytes_stat,
-                                                          int stages, int accumulate) {
+                                                          int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FfnBatch batch;
   __shared__ Plan plan;
@@ -761,10 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
         acc[m] = 0.f;
       }
       consumer_sync();
-      if (ctid < tm.nr) {
-        const float v = (part[ctid][0] + part[ctid][1]) + part[ctid][2];
-        y[tm.r0 + ctid] = accumulate ? y[tm.r0 + ctid] + v : v;
-      }
+      if (ctid < tm.nr) y[tm.r0 + ctid] = (part[ctid][0] + part[ctid][1]) + part[ctid][2];
       consumer_sync();
       --subs_left;
     }
@@ -826,11 +823,11 @@ cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s
 
 cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
                               int max_total_I, cudaStream_t s) {
-  return launch_ffn_decode_engine(batch_dev, xlay, alay, y_dev, H, max_total_I, nullptr, 0, s);
+  return launch_ffn_decode_engine(batch_dev, xlay, alay, y_dev, H, max_total_I, nullptr, s);
 }
 
 cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
-                                     int max_total_I, unsigned long long *bytes_stat, int accumulate, cudaStream_t s) {
+                                     int max_total_I, unsigned long long *bytes_stat, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = ffn_preload();
@@ -845,11 +842,11 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
   // the grid barrier needs every CTA resident: one CTA per SM, grid = #SMs
   const float4 *xl = reinterpret_cast<const float4 *>(xlay);
   if (H == 2048)
-    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, accumulate);
+    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
   else if (H == 4096)
-    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, accumulate);
+    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
   else
-    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, accumulate);
+    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
   return cudaGetLastError();
 }
 
