@@ -140,7 +140,8 @@ __device__ __forceinline__ void word_dot(uint32_t w, const float4 (&xv)[4], floa
     a0 = ffma2(fsub2(make_float2(mag<0>(w), mag<1>(w)), m), lo2(xv[0]), a0);
     a1 = ffma2(fsub2(make_float2(mag<2>(w), mag<3>(w)), m), hi2(xv[0]), a1);
   } else if constexpr (BITS == 4) {
-    const uint32_t lo = w & 0x0F0F0F0Fu, hi = (w >> 4) & 0x0F0F0F0Fu;  // elements 2k | 2k+1 in byte k
+    // elements 2k | 2k+1 in byte k; the shift runs on the FMA pipe (IMAD.HI), the ALU pipe is the bound
+    const uint32_t lo = w & 0x0F0F0F0Fu, hi = __umulhi(w, 1u << 28) & 0x0F0F0F0Fu;
     a0 = ffma2(fsub2(make_float2(mag<0>(lo), mag<0>(hi)), m), lo2(xv[0]), a0);
     a1 = ffma2(fsub2(make_float2(mag<1>(lo), mag<1>(hi)), m), hi2(xv[0]), a1);
     a0 = ffma2(fsub2(make_float2(mag<2>(lo), mag<2>(hi)), m), lo2(xv[1]), a0);
