@@ -22,6 +22,7 @@
 //    FFMA per weight element plus code extraction.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "fate_internal.cuh"
@@ -29,8 +30,10 @@
 namespace fate {
 namespace {
 
-constexpr int kConsumers = 12;  // 13 warps -> 128 registers per thread (allocation in 4-warp units)
-constexpr int kThreads = 32 * (1 + kConsumers);
+constexpr int kConsumers = 12;  // consumer warps
+constexpr int kProducers = 4;   // producer warps (tile g of the stage sequence -> warp g % kProducers);
+                                // 16 warps -> 128 registers per thread (allocation in 4-warp units)
+constexpr int kThreads = 32 * (kProducers + kConsumers);
 constexpr int kStageBytes = 32 * 1024;
 constexpr int kMaxStages = 6;
 constexpr int kSubRows = 16;     // phase B rows per sub-block (r = 4m + warp%4, m < 4)
@@ -366,22 +369,32 @@ __device__ __forceinline__ void up_pair(const uint8_t *__restrict__ tile, int R,
   }
 }
 
-// Phase B: chunk c of a tile (global chunk cg of expert j's activation layout
-// `at`, nchI chunks per activation quad row) for MR rows of the tile,
-// row[i] = 4 m_i + w4, valid[i] = row exists; out[i] = w_j * dot(row[i]).
-template <int BITS, int MR>
-__device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, int c, const float4 *__restrict__ at,
-                                           int nchI, int cg, const int (&row)[MR], int valid, float wj,
-                                           float (&out)[MR]) {
+// Phase B: unit (c, h) of a tile -- words [h*U, h*U+U) of 16-byte chunk c
+// (global chunk cg of expert j's activation layout `at`, nchI chunks per
+// activation quad row) -- for MR rows of the tile, row[i] = 4 m_i + w4,
+// valid[i] = row exists; out[i] = w_j * dot(row[i]).  Quantized tiles with few
+// chunks per row use U = 2 or 1 so that the units still cover all 3 chunk groups.
+template <int BITS, int MR, int U>
+__device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, int c, int h,
+                                           const float4 *__restrict__ at, int nchI, int cg, const int (&row)[MR],
+                                           int valid, float wj, float (&out)[MR]) {
   const int rowb = nc * BITS / 8;
   uint4 q[MR];
 #pragma unroll
-  for (int i = 0; i < MR; ++i)
-    q[i] = (valid >> i & 1) ? reinterpret_cast<const uint4 *>(tile + row[i] * rowb)[c] : make_uint4(0, 0, 0, 0);
+  for (int i = 0; i < MR; ++i) {
+    const uint8_t *src = tile + row[i] * rowb + c * 16 + h * 4 * U;
+    if (!(valid >> i & 1)) q[i] = make_uint4(0, 0, 0, 0);
+    else if constexpr (U == 4) q[i] = *reinterpret_cast<const uint4 *>(src);
+    else if constexpr (U == 2) {
+      const uint2 t = *reinterpret_cast<const uint2 *>(src);
+      q[i] = make_uint4(t.x, t.y, 0, 0);
+    } else q[i] = make_uint4(*reinterpret_cast<const uint32_t *>(src), 0, 0, 0);
+  }
   float2 p[MR][2];
 #pragma unroll
   for (int i = 0; i < MR; ++i) p[i][0] = p[i][1] = make_float2(0.f, 0.f);
   if constexpr (BITS == 16) {
+    static_assert(U == 4, "bf16 tiles use whole chunks");
     const float4 x0 = at[cg], x1 = at[nchI + cg];
 #pragma unroll
     for (int i = 0; i < MR; ++i) {
@@ -396,12 +409,14 @@ __device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, 
     constexpr int qpw = 32 / BITS / 4;
     float2 sa = make_float2(0.f, 0.f);
     float4 xv[4];
-#define FATE_WORD(WI)                                                   \
-  _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                  \
-    xv[qi] = at[((WI) * qpw + qi) * nchI + cg];                         \
-    sa = fadd2(sa, fadd2(lo2(xv[qi]), hi2(xv[qi])));                    \
-  }                                                                     \
-  _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]);
+#define FATE_WORD(WI)                                                      \
+  if constexpr ((WI) < U) {                                                \
+    _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                   \
+      xv[qi] = at[((h * U + (WI)) * qpw + qi) * nchI + cg];                \
+      sa = fadd2(sa, fadd2(lo2(xv[qi]), hi2(xv[qi])));                     \
+    }                                                                      \
+    _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]); \
+  }
     FATE_WORD(0) FATE_WORD(1) FATE_WORD(2) FATE_WORD(3)
 #undef FATE_WORD
     const float xsum = sa.x + sa.y;
@@ -419,12 +434,13 @@ __device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, 
 
 // Rows of a phase B tile owned by consumer warp cw (12 warps): with 3 chunk
 // groups (G = 3) warp cw takes chunk group cw / 4 and rows r = 4m + cw % 4
-// (m = 0..3); with one group (G = 1, at most 32 chunks per row) it takes rows
+// (m = 0..3); with one group (G = 1, at most 32 units per row) it takes rows
 // cw and cw + 12.  Either way r = 4m + (cw & 3), so every thread's rows stay in
 // acc[m] for the whole sub-block whatever the tile's chunk-group count.
-template <int BITS, int MR>
-__device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, int c, const float4 *__restrict__ at,
-                                          int nchI, int cg, int cw, float wj, float (&acc)[4]) {
+template <int BITS, int MR, int U>
+__device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, int c, int h,
+                                          const float4 *__restrict__ at, int nchI, int cg, int cw, float wj,
+                                          float (&acc)[4]) {
   int m[MR], row[MR], valid = 0;
 #pragma unroll
   for (int i = 0; i < MR; ++i) {
@@ -433,7 +449,7 @@ __device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, i
     if (row[i] < nr) valid |= 1 << i;
   }
   float out[MR];
-  down_chunk<BITS, MR>(tile, nr, nc, c, at, nchI, cg, row, valid, wj, out);
+  down_chunk<BITS, MR, U>(tile, nr, nc, c, h, at, nchI, cg, row, valid, wj, out);
 #pragma unroll
   for (int i = 0; i < MR; ++i) {
     if constexpr (MR == 4) {
@@ -445,20 +461,36 @@ __device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, i
   }
 }
 
-// One phase B tile: the 12 consumer warps split the tile's chunks into G
-// groups of 32 lanes (G = 1 or 3) and its rows into 12 / G residue classes.
+template <int BITS, int U>
+__device__ __forceinline__ void down_tile_units(const TileMeta &tm, const uint8_t *tile, const FfnExpert &ex,
+                                                const float *al_j, int cw, int lane, int nch, float (&acc)[4]) {
+  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;  // columns per 16-byte chunk
+  const int nunits = nch * (4 / U);
+  const bool g3 = nunits > 32;
+  const int u = lane + (g3 ? 32 * (cw >> 2) : 0);
+  if (u >= nunits) return;
+  const int c = u / (4 / U), h = u % (4 / U);
+  const float4 *at = reinterpret_cast<const float4 *>(al_j);
+  const int nchI = ex.I / cols, cg = tm.k0 / cols + c;
+  if (g3) down_tile<BITS, 4, U>(tile, tm.nr, tm.nc, c, h, at, nchI, cg, cw, ex.weight, acc);
+  else down_tile<BITS, 2, U>(tile, tm.nr, tm.nc, c, h, at, nchI, cg, cw, ex.weight, acc);
+}
+
+// One phase B tile: the 12 consumer warps split the tile's units (chunks, or
+// half / quarter chunks of quantized rows with <= 48 / 24 chunks) into G groups
+// of 32 lanes (G = 1 or 3) and its rows into 12 / G residue classes.
 template <int BITS>
 __device__ __forceinline__ void down_tile_bits(const TileMeta &tm, const uint8_t *tile, const FfnExpert &ex,
                                                const float *al_j, int cw, int lane, float (&acc)[4]) {
-  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;  // columns per 16-byte chunk
+  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;
   const int nch = tm.nc / cols;
-  const bool g3 = nch > 32;
-  const int c = lane + (g3 ? 32 * (cw >> 2) : 0);
-  if (c >= nch) return;
-  const float4 *at = reinterpret_cast<const float4 *>(al_j);
-  const int nchI = ex.I / cols, cg = tm.k0 / cols + c;
-  if (g3) down_tile<BITS, 4>(tile, tm.nr, tm.nc, c, at, nchI, cg, cw, ex.weight, acc);
-  else down_tile<BITS, 2>(tile, tm.nr, tm.nc, c, at, nchI, cg, cw, ex.weight, acc);
+  if constexpr (BITS == 16) {
+    down_tile_units<16, 4>(tm, tile, ex, al_j, cw, lane, nch, acc);
+  } else {
+    if (nch > 48) down_tile_units<BITS, 4>(tm, tile, ex, al_j, cw, lane, nch, acc);
+    else if (nch > 24) down_tile_units<BITS, 2>(tm, tile, ex, al_j, cw, lane, nch, acc);
+    else down_tile_units<BITS, 1>(tm, tile, ex, al_j, cw, lane, nch, acc);
+  }
 }
 
 // One launch per decode step:
@@ -479,7 +511,7 @@ template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
                                                           const float4 *__restrict__ xlay, float *__restrict__ alay,
                                                           float *__restrict__ y, unsigned long long *bytes_stat,
-                                                          int stages) {
+                                                          int stages, int nprod) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FfnBatch batch;
   __shared__ Plan plan;
@@ -518,9 +550,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
   uint8_t *ring_buf = smem;
   float4 *xl = reinterpret_cast<float4 *>(smem + (size_t)stages * kStageBytes);  // x layouts (phase A)
   float *al = reinterpret_cast<float *>(xl);                                      // activation layouts (phase B)
-  if (warp == 0) {
-    // ================= producer warp: lane 0 arms stages, lanes issue copies
-    if (lane == 0) {
+  if (warp < kProducers) {
+    // ================= producer warps: tile g of the stage sequence (phase A
+    // tiles, end marker, phase B tiles) belongs to producer g % kProducers, so
+    // the ~0.1 us issue latency of each bulk copy overlaps across warps.  The
+    // ring has more stages than producers, so an empty-barrier parity never aliases.
+    const int pw = warp;
+    if (pw == 0 && lane == 0) {
       const uint32_t xbytes = (uint32_t)(4 * lay_stride * 16);
       mbar_expect_tx(&x_bar, xbytes);
       bulk_g2s(xl, xlay, xbytes, &x_bar);
@@ -530,13 +566,24 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
         atomicAdd(bytes_stat, bytes);
       }
     }
-    int stage = 0, ti = 0;
+    // active producers: fewer than the ring's stages (parity safety)
+    const int np = nprod < stages - 1 ? nprod : stages - 1;
+    if (pw >= np) return;
+    int stage = 0, ti = 0;  // ti = position in the stage sequence
     uint32_t phase = 0;
+    auto mine = [&]() -> bool {
+      stage = ti % stages;
+      phase = (uint32_t)(ti / stages) & 1u;
+      return ti % np == pw;
+    };
     // one phase A tile (or the end marker); returns true at the end
     auto step_a = [&](int t) -> bool {
+      if (!mine()) {
+        ++ti;
+        return t >= plan.n_a;
+      }
       K3_TRACE(0, ti, 0);
       mbar_wait(&ring.empty[stage], phase ^ 1);
-      K3_TRACE(0, ti, 1);
       const bool end = t >= plan.n_a;
       if (end) {
         if (lane == 0) {
@@ -560,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
           mbar_expect_tx(&ring.full[stage], 2 * (cb + sb));
         }
         __syncwarp();
+        K3_TRACE(0, ti, 1);
         if (lane < (sb ? 4 : 2)) {
           // lanes 0..3: W1 codes, W3 codes, W1 (scale, zero), W3 (scale, zero)
           const int64_t n = (int64_t)H * ex.I, cbytes = bits == 16 ? 2 * n : n * bits / 8;
@@ -574,7 +622,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       }
       K3_TRACE(0, ti, 2);
       ++ti;
-      if (++stage == stages) stage = 0, phase ^= 1;
       return end;
     };
     // static round-robin over the tile list (expert-major, so every CTA gets a
@@ -607,12 +654,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
           const Layout L = make_layout(H, ex.I, bits);
           const int64_t rb = L.row_bytes_down, szb = sz_row_bytes(ex.I, bits);
           const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
-          {
+          if (!mine()) {
+            ++ti;
+          } else {
             const int k0 = kt * plan.colsB[j], nc = min(plan.colsB[j], ex.I - k0);
             const uint32_t cb = (uint32_t)nc * bits / 8, sb = bits == 16 ? 0u : (uint32_t)nc / 8;
             K3_TRACE(0, ti, 0);
             mbar_wait(&ring.empty[stage], phase ^ 1);
-            K3_TRACE(0, ti, 1);
             uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
             if (lane == 0) {
               TileMeta &m = meta[stage];
@@ -625,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
               mbar_expect_tx(&ring.full[stage], (uint32_t)nr * (cb + sb));
             }
             __syncwarp();
+            K3_TRACE(0, ti, 1);
             if (ex.layout == 1) {
               // bf16 W2 in column slabs (kSlabCols == this K-range): the tile's rows are contiguous
               if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)H * k0 * 2 + (int64_t)rs0 * nc * 2,
@@ -641,25 +690,24 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
             }
             K3_TRACE(0, ti, 2);
             ++ti;
-            if (++stage == stages) stage = 0, phase ^= 1;
           }
         }
       }
     }
-    if (lane == 0) prof[7] = gtime();
+    if (lane == 0 && pw == 0) prof[7] = gtime();
     return;
   }
   // ================= consumers
-  const int ctid = tid - 32, cw = warp - 1;
+  const int ctid = tid - 32 * kProducers, cw = warp - kProducers;
   if (ctid == 0) prof[1] = gtime();
   mbar_wait(&x_bar, 0);  // x layouts landed
   if (ctid == 0) prof[2] = gtime();
   int stage = 0, k = 0, rot = 0;
   uint32_t phase = 0;
   for (;; ++k) {
-    K3_TRACE(warp, k, 0);
+    K3_TRACE(cw + 1, k, 0);
     mbar_wait(&ring.full[stage], phase);
-    K3_TRACE(warp, k, 1);
+    K3_TRACE(cw + 1, k, 1);
     const int j = meta[stage].j;
     if (j < 0) {
       __syncwarp();
@@ -707,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     rot = (rot + nr) % kConsumers;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[stage]);
-    K3_TRACE(warp, k, 2);
+    K3_TRACE(cw + 1, k, 2);
     if (++stage == stages) stage = 0, phase ^= 1;
   }
   // ---- every CTA's activations are complete and visible
@@ -732,9 +780,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
   for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x)
     subs_left += (min(plan.RBB, H - blk * plan.RBB) + kSubRows - 1) / kSubRows;
   while (subs_left > 0) {
-    K3_TRACE(warp, k, 0);
+    K3_TRACE(cw + 1, k, 0);
     mbar_wait(&ring.full[stage], phase);
-    K3_TRACE(warp, k, 1);
+    K3_TRACE(cw + 1, k, 1);
     const TileMeta tm = meta[stage];
     const FfnExpert &ex = batch.e[tm.j];
     mbar_wait(&act_bar[tm.j], 0);
@@ -750,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[stage]);
-    K3_TRACE(warp, k, 2);
+    K3_TRACE(cw + 1, k, 2);
     ++k;
     if (++stage == stages) stage = 0, phase ^= 1;
     if (tm.flush) {
@@ -838,16 +886,21 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
   const int sms = num_sms();
   const size_t extra = region_bytes(H, max_total_I);
   const int st = stages_for(extra);
+  static const int nprod = [] {
+    const char *e = getenv("FATE_K3_PRODUCERS");  // tuning knob: producer warps actually issuing (1..4)
+    const int v = e ? atoi(e) : kProducers;
+    return v < 1 ? 1 : v > kProducers ? kProducers : v;
+  }();
   const size_t smem = (size_t)st * kStageBytes + extra;
   if (smem + kStaticReserve > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
   // the grid barrier needs every CTA resident: one CTA per SM, grid = #SMs
   const float4 *xl = reinterpret_cast<const float4 *>(xlay);
   if (H == 2048)
-    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
+    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
   else if (H == 4096)
-    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
+    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
   else
-    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st);
+    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
   return cudaGetLastError();
 }
 

@@ -93,7 +93,7 @@ def test_pack_expert_layout(bits):
 
 
 @pytest.mark.parametrize("H,I,bits_list", [(256, 512, [4, 2]), (2048, 1408, [4, 4, 2, 4]), (2048, 1408, [16]),
-                                            (4096, 1024, [8, 2])])
+                                            (4096, 1024, [8, 2]), (2048, 5632, [4, 2])])
 def test_ffn_decode_numerics(H, I, bits_list):
     torch = _torch()
     from paper_2502_12224_b200 import ops

@@ -109,7 +109,7 @@ def print_k3_trace(_lib, mhz=1965.0):
         if sub[t, 0] > 0:
             print(f"  sub tile {t}: dots done {(sub[t,0]-t0)/mhz:7.2f} sums {(sub[t,1]-t0)/mhz:7.2f} "
                   f"store {(sub[t,2]-t0)/mhz:7.2f}")
-    print("CTA0 trace (us): producer [wait-start empty-passed issued] | consumer w1 [wait full released] | "
+    print("CTA0 trace (us): producer [wait-start pre-copy issued] | consumer w1 [wait full released] | "
           "max over consumers of release")
     for t in range(48):
         if np.all(np.isnan(us[:, t, :])):
