@@ -179,13 +179,21 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   __shared__ int32_t tchosen[KMAX];
   const int E = d.E, H = d.H, L = d.L;
   const double *h = gate_in + ((int64_t)token * L + layer) * H;
-  // block 0: the tail (stages state while the others work), blocks
-  // 1..n_rows: router rows, last block: the deferred ARC update
-  // block 0: the tail; blocks 1..n_rows: router rows.  The previous step's
-  // deferred update_after_layer ran in arc_update_kernel on the side stream
-  // (overlapping that step's transfers and K3) and completed before this launch.
-  const int n_rows = gridDim.x - 1;
+  // block 0: the tail (stages state while the others work); blocks
+  // 1..n_rows: router rows; last block: the FFN input x and its K3 layouts.
+  // The previous step's deferred update_after_layer ran in arc_update_kernel
+  // on the side stream (overlapping that step's transfers and K3) and
+  // completed before this launch.
+  const int n_rows = gridDim.x - 2;
   const int row = blockIdx.x - 1;
+  if (blockIdx.x == gridDim.x - 1) {
+    // FFN input x = sqrt(H) * gate_in (fp64 product, fp32 storage) -> K3 layouts
+    const double sH = sqrt((double)H);
+    for (int i = threadIdx.x; i < H; i += kGateThreads) S.xs[i] = (float)(sH * h[i]);
+    __syncthreads();
+    write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
+    return;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_prof[0] = gtime1();
   if (threadIdx.x == 0 && blockIdx.x == 1) g_k1_prof[10] = gtime1();
   if (blockIdx.x > 0) {
@@ -230,17 +238,12 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (threadIdx.x == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(&d.ctrl->arrive, 1u);
-      if (prev == gridDim.x - 2) g_k1_prof[11] = gtime1();  // last arrival
+      if (prev == (unsigned)n_rows - 1u) g_k1_prof[11] = gtime1();  // last arrival
     }
     return;
   }
   // ================= tail block
   Ctrl &C = *d.ctrl;
-  // ---- FFN input x = sqrt(H) * gate_in (fp64 product, fp32 storage)
-  const double sH = sqrt((double)H);
-  for (int i = threadIdx.x; i < H; i += kGateThreads) S.xs[i] = (float)(sH * h[i]);
-  __syncthreads();
-  write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
   // stage every table the tail reads while the router rows are in flight
   const int pl = C.prev_valid ? C.prev_layer : -1;  // layer the ARC block is editing
   for (int i = threadIdx.x; i < E; i += kGateThreads) {
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     S.c_pred_n = C.pred_n;
     S.shared_present = d.shared && d.shared[layer] ? 1 : 0;
     // wait for the router rows and the ARC block
-    while (*(volatile uint32_t *)&C.arrive < (uint32_t)(gridDim.x - 1)) {
+    while (*(volatile uint32_t *)&C.arrive < (uint32_t)n_rows) {
     }
     __threadfence();
     g_k1_prof[1] = gtime1();
@@ -487,9 +490,10 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (all_landed) ready_host[layer] = (uint32_t)token + 1u;
   }
   __syncwarp();
-  __threadfence_system();
   if (lane == 0) {
-    msg->seq = (uint32_t)step + 1u;
+    // publish: every lane's message fields (ordered by __syncwarp) before seq,
+    // system scope (the host polls the mapped ring)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&msg->seq), "r"((uint32_t)step + 1u) : "memory");
     // (9) control block for the next step
     C.prev_valid = 1;
     C.prev_layer = layer;
@@ -500,7 +504,6 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     C.step = step + 1;
     if (layer == L - 1) C.next_token = token + 1;
     g_k1_prof[6] = gtime1();
-    __threadfence();
     g_k1_prof[7] = gtime1();
   }
 }
@@ -1322,7 +1325,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       const int s = launched, t = s / L, l = s % L;
       // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
       // tail block + router rows of W_l (and W_{l+1} when predicting)
-      const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 1;
+      const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
       FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));  // previous step's ARC update applied
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
       decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
