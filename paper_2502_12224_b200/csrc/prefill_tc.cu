@@ -206,8 +206,14 @@ struct Item {
 
 // Items are expert-major: for e, for token tile, for row tile.
 __device__ __forceinline__ Item item_of(const int *pref, const int *nrt, int n, int idx) {
-  int e = 0;
-  while (idx >= pref[e + 1]) ++e;
+  // largest e with pref[e] <= idx (binary search; pref is non-decreasing, pref[n] > idx)
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pref[mid] <= idx) lo = mid;
+    else hi = mid - 1;
+  }
+  const int e = lo;
   const int local = idx - pref[e];
   return Item{e, local / nrt[e], local % nrt[e]};
 }
