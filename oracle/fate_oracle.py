@@ -331,6 +331,21 @@ class StrategyKnobs:
         return 2 if self.quant else 16
 
 
+def eap_list(counts_l: np.ndarray, chosen, k: int) -> list[int]:
+    """eap_predict (predict.py:138-158): Laplace-smoothed, row-normalised
+    co-activation scores summed over the chosen set in ascending id order,
+    top-k by (-score, id); cold start (every relevant row empty) -> 0..k-1."""
+    E = counts_l.shape[1]
+    ch = sorted(int(a) for a in chosen)
+    totals = {a: int(counts_l[a].sum()) for a in ch}
+    if all(v == 0 for v in totals.values()):
+        return list(range(k))
+    score = np.zeros(E)
+    for a in ch:
+        score += (counts_l[a] + 1.0) / (totals[a] + E)
+    return sorted(range(E), key=lambda e: (-score[e], e))[:k]
+
+
 def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
                     knobs: StrategyKnobs, cached_bits: int, arcs: list | None = None) -> dict:
     """Timing-independent fields of simulate_decoding (pipeline.py:343-517).
@@ -349,6 +364,9 @@ def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
     recall_sum, recall_n, dequant = 0.0, 0, 0
     cache_hits = 0
     use_pred = knobs.kind == "fate"
+    use_eap = knobs.kind == "eap"
+    E = int(np.asarray(mats).shape[1])
+    counts = np.zeros((max(L - 1, 1), E, E), dtype=np.int64)  # EapStats (predict.py:110-130)
     for t in range(T):
         for l in range(L):
             rec = {"token": t, "layer": l}
@@ -362,6 +380,20 @@ def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
                 rec["prefetch"] = iss
             ch = sorted(int(e) for e in chosen[t][l])
             rec["chosen"] = ch
+            if use_eap:
+                # observe (pipeline.py:310-315, eap_update predict.py:132-138), then
+                # predict l+1 from l's chosen set at gate end (pipeline.py:421-428)
+                if l > 0:
+                    prev = sorted(int(e) for e in chosen[t][l - 1])
+                    for a in prev:
+                        counts[l - 1, a, ch] += 1
+                if l + 1 < L:
+                    lst = eap_list(counts[l], ch, k)[:budget_n]
+                    pred_sets[(t, l + 1)] = set(lst)
+                    iss = [e for e in lst if e not in arcs[l + 1].resident()]
+                    issued[(t, l + 1)] = iss
+                    rec["pred"] = lst
+                    rec["prefetch"] = iss
             if (t, l) in pred_sets:
                 recall_sum += len(pred_sets.pop((t, l)) & set(ch)) / len(ch)
                 recall_n += 1

@@ -127,6 +127,13 @@ class LogPredictor(mpipe.CrossLayerDecodePredictor):
         return pl
 
 
+class LogEapPredictor(mpipe.EapDecodePredictor):
+    def predict(self, token, source_layer, record, chosen):
+        pl = super().predict(token, source_layer, record, chosen)
+        LOG.setdefault("pred", []).append((token, source_layer + 1, list(pl.experts())))
+        return pl
+
+
 def arc_states(cache):
     return [{"t1": list(a.t1), "t2": list(a.t2), "b1": list(a.b1), "b2": list(a.b2), "p": float(a.p_arc)}
             for a in cache.layers]
@@ -140,7 +147,12 @@ def report_dict(rep):
 def run_decode_logged(trace, strategy, plan, timing, cfg, weights, cache):
     LOG.clear()
     mpipe._Channel = LogChannel
-    pred = LogPredictor(weights, strategy.prefetch_policy, cfg.top_k) if strategy.kind == "fate" else None
+    if strategy.kind == "fate":
+        pred = LogPredictor(weights, strategy.prefetch_policy, cfg.top_k)
+    elif strategy.kind == "eap":
+        pred = LogEapPredictor(cfg.num_layers, cfg.num_experts, cfg.top_k)
+    else:
+        pred = None
     tl, rep = mpipe.simulate_decoding(trace, strategy, plan, timing, cfg, weights=weights, cache=cache,
                                       predictor=pred, collect_cache_events=True)
     n = mpipe.transfer_budget(timing, strategy.prefetch_bits())
@@ -207,6 +219,19 @@ def dump_trace_arrays(trace, cfg):
             g[t, l] = r.probe_hidden["gate_in_cur"]
             ch[t, l] = sorted(r.chosen)
     return g, ch
+
+
+def eap_entries(sched):
+    """EAP baseline decode (pipeline.py:301-321, predict.py:110-158) from a cold cache."""
+    for name in ("tiny", "qwen"):
+        c = CONFIGS[name]
+        cfg = model_cfg(c)
+        dec, pre, w = traces_for(cfg, c)
+        timing = mcore.TimingModel(**PAPER_TIMING)
+        budget = cfg.dense_bytes + c["S"] * cfg.expert_bytes[4]
+        plan = mcache.plan_allocation(cfg, budget, 4)
+        cache = LogCache(plan)
+        sched[name]["decode_eap"] = run_decode_logged(dec, mpipe.Strategy.eap(), plan, timing, cfg, w, cache)
 
 
 def main():
@@ -316,6 +341,7 @@ def main():
             entry["decode_lod"] = run_decode_logged(dec, mpipe.Strategy.lod(), lod_plan, timing, cfg, w, cache)
         print(name, "decode hit", entry["decode_cold"]["report"]["hit_rate"],
               "prefill", entry["prefill_cold"]["report"]["tokens_per_s"], flush=True)
+    eap_entries(sched)
     golden["schedules"] = sched
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
         json.dump(golden, fh, separators=(",", ":"))

@@ -87,18 +87,31 @@ def _arrays(trace, cfg):
     return g, ch.tolist()
 
 
-@pytest.mark.parametrize("variant", ["decode_cold", "decode_cold_n0", "decode_cold_topk", "decode_lod"])
+@pytest.mark.parametrize("variant", ["decode_cold", "decode_cold_n0", "decode_cold_topk", "decode_lod", "decode_eap"])
 def test_tiny_decode_schedule(variant):
     e = golden()["schedules"]["tiny"]
     tr = tiny_traces()
     mats, taus = tr["gate_w"], tr["taus"]
     want = e[variant]
-    kind = "lod" if variant == "decode_lod" else "fate"
+    kind = {"decode_lod": "lod", "decode_eap": "eap"}.get(variant, "fate")
     knobs = _knobs(kind=kind, quant=kind == "fate",
-                   policy_kind="topk" if variant.endswith("topk") else "percentile")
+                   policy_kind="topk" if variant.endswith("topk") or kind == "eap" else "percentile")
     caps = [0] * 4 if kind == "lod" else e["plan"]
     got = O.decode_schedule(tr["dec_gate_in"], tr["dec_chosen"].tolist(), mats, taus, caps, 2, want["n"],
-                            knobs, 4 if kind == "fate" else 16)
+                            knobs, 16 if kind == "lod" else 4)
+    _check_decode(got, want)
+
+
+def test_qwen_eap_decode_schedule():
+    """EAP baseline (pipeline.py:301-321) on the Qwen shape: co-activation stats
+    accumulate over tokens, so later steps exercise the scored (non-cold) path."""
+    from golden_util import config_traces
+    e = golden()["schedules"]["qwen"]
+    want = e["decode_eap"]
+    cfg, dec, pre, w = config_traces("qwen")
+    g, ch = _arrays(dec, cfg)
+    got = O.decode_schedule(g, ch, np.stack(w.matrices), np.array(w.temperatures), e["plan"], cfg.top_k, want["n"],
+                            _knobs(kind="eap", quant=False, policy_kind="topk"), 4)
     _check_decode(got, want)
 
 
