@@ -144,7 +144,7 @@ typedef struct fate_engine_config {
   int prefetch_bits;             /* Strategy.prefetch_bits()   (pipeline.py:96-97)  */
   int ondemand_bits;             /* Strategy.ondemand_bits()   (pipeline.py:99-101) */
   int use_predictor;             /* fate: 1, lod: 0                         */
-  int policy;                    /* 0 topk, 1 percentile (predict.py:21-47) */
+  int policy;                    /* 0 topk, 1 percentile (predict.py:21-47), 2 EAP co-activation (predict.py:110-158, decode) */
   double percentile_q;
   int budget_n;                  /* transfer_budget (pipeline.py:151-156)   */
   int prefill_use_predictor;     /* fate prefill prediction (pipeline.py:568) */

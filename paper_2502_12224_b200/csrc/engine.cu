@@ -163,6 +163,7 @@ struct TailSmem {
   uint32_t pgen_l[EMAX], pdone_l[EMAX];
   int32_t pred_prev[EMAX];
   int32_t c_free_top, c_step, c_pred_valid, c_pred_layer, c_pred_n, shared_present;
+  int32_t eap_prev[KMAX], eap_prev_ok;
   double z[2 * EMAX], w[2 * EMAX];
   int32_t ord[2 * EMAX];
   int32_t chosen[KMAX], cbuf[KMAX], csrc[KMAX], chit[KMAX], carr[KMAX];
@@ -260,11 +261,15 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (pl != layer + 1) S.bof_n[i] = layer + 1 < L ? d.buf_of[(layer + 1) * E + i] : 0;
   }
   if (threadIdx.x < d.k && trace_chosen) tchosen[threadIdx.x] = trace_chosen[((int64_t)token * L + layer) * d.k + threadIdx.x];
+  if (threadIdx.x < KMAX) S.eap_prev[threadIdx.x] = threadIdx.x < C.prev_k ? C.prev_chosen[threadIdx.x] : 0;
   if (threadIdx.x == 0) {
     S.c_step = C.step;
     S.c_pred_valid = C.pred_valid;
     S.c_pred_layer = C.pred_layer;
     S.c_pred_n = C.pred_n;
+    // EAP observe needs the chosen set of (token, layer - 1): the previous step
+    // (prev_valid is cleared once the deferred ARC update ran; the chosen set stays)
+    S.eap_prev_ok = layer > 0 && C.step > 0 && C.prev_layer == layer - 1 ? 1 : 0;
     S.shared_present = d.shared && d.shared[layer] ? 1 : 0;
     // wait for the router rows and the ARC block
     while (*(volatile uint32_t *)&C.arrive < (uint32_t)n_rows) {
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   for (int i = threadIdx.x; i < S.c_pred_n; i += kGateThreads) S.pred_prev[i] = C.pred_list[i];
   // (2) routing of layer l and the cross-layer prediction for l+1: the two
   // softmaxes on warps 0 and 1 at once, then the ranks by the whole block
-  const bool pred_seg = d.use_predictor && layer + 1 < L;
+  const bool pred_seg = d.use_predictor && d.policy != 2 && layer + 1 < L;
   if ((threadIdx.x >> 5) == 0) warp_softmax(S.z, S.w, E);
   else if ((threadIdx.x >> 5) == 1 && pred_seg) warp_softmax(S.z + E, S.w + E, E);
   __syncthreads();
@@ -409,8 +414,41 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (lane == 0) g_k1_prof[4] = gtime1();
   // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
   int n_pf = 0, n_pred = -1;
+  if (d.use_predictor && d.policy == 2) {
+    // EAP observe (pipeline.py:310-315, eap_update predict.py:132-138): every
+    // (a, b) in chosen(l-1) x chosen(l) -> counts[l-1][a][b] += 1 (distinct pairs)
+    if (S.eap_prev_ok) {
+      int32_t *cnt = d.eap_counts + (int64_t)(layer - 1) * E * E;
+      for (int i = lane; i < k * k; i += 32) cnt[S.eap_prev[i / k] * E + S.chosen[i % k]] += 1;
+      if (lane < k) d.eap_totals[(layer - 1) * E + S.eap_prev[lane]] += k;
+    }
+    // EAP predict for l+1 (eap_predict predict.py:141-158): Laplace-smoothed
+    // row-normalised scores summed over chosen(l) in ascending id order
+    // (fp64, IEEE division as numpy), top-k by (-score, id); cold start 0..k-1
+    if (layer + 1 < L) {
+      const int32_t *cnt = d.eap_counts + (int64_t)layer * E * E;
+      const int32_t *tot = d.eap_totals + (int64_t)layer * E;
+      int warm = 0;
+      for (int j = 0; j < k; ++j) warm |= tot[S.chosen[j]] != 0;
+      if (!warm) {
+        for (int e = lane; e < E; e += 32) S.ord[E + e] = e;
+      } else {
+        for (int e = lane; e < E; e += 32) {
+          double sc = 0.0;
+          for (int j = 0; j < k; ++j) {
+            const int a = S.chosen[j];
+            sc = __dadd_rn(sc, __ddiv_rn((double)cnt[a * E + e] + 1.0, (double)(tot[a] + E)));
+          }
+          S.w[E + e] = sc;
+        }
+        __syncwarp();
+        rank_by_weight(S.w + E, S.ord + E, E, lane, 32);
+      }
+      __syncwarp();
+    }
+  }
   if (d.use_predictor && layer + 1 < L) {
-    const int len = warp_pred_len(S.w + E, S.ord + E, E, k, d.policy, d.q);  // S.w / S.ord + E above
+    const int len = d.policy == 2 ? (k < E ? k : E) : warp_pred_len(S.w + E, S.ord + E, E, k, d.policy, d.q);
     n_pred = len < d.budget_n ? len : d.budget_n;
     for (int base = 0; base < n_pred; base += 32) {
       const int i = base + lane;
@@ -667,6 +705,7 @@ struct fate_engine {
   StepMsg *ring_host = nullptr;
   volatile uint32_t *ready_host = nullptr;     // [L]
   uint32_t *ready_dev = nullptr;
+  size_t eap_bytes = 0;  // eap_counts .. end of eap_totals (contiguous in dev_block)
   volatile uint32_t *copy_done_host = nullptr, *copy_done_host2 = nullptr;  // per copy stream
   CUdeviceptr copy_done_dev = 0, copy_done_dev2 = 0;
   // host pools
@@ -711,8 +750,8 @@ int check_cfg(const fate_engine_config *c) {
     set_error("fate_engine_create: bit widths must be 2, 4, 8 or 16");
     return FATE_EINVAL;
   }
-  if (c->policy != 0 && c->policy != 1) {
-    set_error("fate_engine_create: policy must be 0 (topk) or 1 (percentile)");
+  if (c->policy != 0 && c->policy != 1 && c->policy != 2) {
+    set_error("fate_engine_create: policy must be 0 (topk), 1 (percentile) or 2 (eap)");
     return FATE_EINVAL;
   }
   for (int l = 0; l < c->num_layers; ++l)
@@ -820,7 +859,8 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
                o_ctrl = carve(sizeof(Ctrl)), o_st = carve(sizeof(DevStats)), o_lg = carve(2 * EMAX * 8),
                o_x = carve(ffn_xlay_floats(H) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
                o_sh = carve((size_t)L * 8), o_sh3 = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
-               o_a = carve(ffn_alay_floats(g->max_total_I) * 4);
+               o_a = carve(ffn_alay_floats(g->max_total_I) * 4),
+               o_ec = carve((size_t)std::max(L - 1, 1) * E * E * 4), o_et = carve((size_t)std::max(L - 1, 1) * E * 4);
   FATE_CUDA(cudaMalloc(&g->dev_block, off));
   FATE_CUDA(cudaMemset(g->dev_block, 0, off));
   uint8_t *base = (uint8_t *)g->dev_block;
@@ -847,6 +887,9 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   d.shared_layout = cfg->shared_bits == 16 ? 1 : 0;
   g->scratch_i = (int32_t *)(base + o_si);
   g->a_scratch = (float *)(base + o_a);
+  d.eap_counts = (int32_t *)(base + o_ec);
+  d.eap_totals = (int32_t *)(base + o_et);
+  g->eap_bytes = (size_t)((o_et - o_ec) + (size_t)std::max(L - 1, 1) * E * 4);
   FATE_CUDA(cudaMalloc(&g->pool, (size_t)nbuf * g->buf_stride));
   d.pool = g->pool;
   FATE_CUDA(cudaMemcpy(g->caps_dev, g->caps.data(), L * 4, cudaMemcpyHostToDevice));
@@ -1269,6 +1312,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   *g->copy_done_host2 = 0;
   for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
   const cudaStream_t cs = g->cstream;
+  // EAP statistics start empty for every decode call (build_decode_predictor, pipeline.py:324-336)
+  if (g->cfg.use_predictor && g->cfg.policy == 2) FATE_CUDA(cudaMemsetAsync(g->d.eap_counts, 0, g->eap_bytes, cs));
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
   run_begin_kernel<<<1, 1, 0, cs>>>(g->d);
   FATE_CHECK_LAUNCH("run_begin_kernel");
@@ -1288,7 +1333,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   };
   int status = FATE_OK;
   auto last_progress = std::chrono::steady_clock::now();
-  const int rows_pred = g->cfg.use_predictor ? 2 : 1;
+  const int rows_pred = g->cfg.use_predictor && g->cfg.policy != 2 ? 2 : 1;  // EAP needs no W_{l+1} rows
   const bool dbg = getenv("FATE_DEBUG") != nullptr;
   auto last_beat = std::chrono::steady_clock::now();
   while (processed < n_steps) {

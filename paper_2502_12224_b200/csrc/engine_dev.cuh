@@ -62,7 +62,9 @@ struct DevStats {
 struct EngineDev {
   int L, E, k, H, I, I_shared, shared_bits;
   int cached_bits, prefetch_bits, ondemand_bits;
-  int use_predictor, policy, budget_n;
+  int use_predictor, policy, budget_n;  // policy: 0 top-k, 1 percentile (cross-layer), 2 EAP
+  int32_t *eap_counts;        // [L-1, E, E] co-activation counts (EapStats, predict.py:110-130)
+  int32_t *eap_totals;        // [L-1, E] their row sums
   double q;
   int nbuf;
   int64_t buf_stride;

@@ -84,7 +84,7 @@ class OffloadEngine:
             intermediate_dim=cfg.intermediate_dim, shared_intermediate=self.store.shared_intermediate,
             shared_bits=self.store.shared_bits, capacity=self._caps_c, cached_bits=k.cached_bits,
             prefetch_bits=k.prefetch_bits, ondemand_bits=k.ondemand_bits, use_predictor=int(k.use_predictor),
-            policy=1 if k.policy == "percentile" else 0, percentile_q=k.percentile_q, budget_n=k.budget_n,
+            policy={"percentile": 1, "eap": 2}.get(k.policy, 0), percentile_q=k.percentile_q, budget_n=k.budget_n,
             prefill_use_predictor=int(k.prefill_use_predictor), reorder_prefill=int(k.reorder_prefill),
             p_int2=k.p_int2, prefill_ondemand_bits=k.prefill_ondemand_bits, max_tokens=self.max_tokens,
             max_inflight=k.max_inflight, device=self.device)

@@ -145,12 +145,12 @@ def default_store(cfg: ModelConfig, bits, shared_intermediate: int = 0, seed: in
 def knobs_for(strategy: Strategy, plan: CachePlan, n: int):
     from .engine import StrategyKnobs
 
-    if strategy.kind == "eap":
-        raise InvalidConfig("the EAP baseline is not implemented on the B200 engine (SURVEY.md §8f rank 2)")
     pol = strategy.prefetch_policy or PrefetchPolicy("topk")
     qp = strategy.quant_policy
+    # eap: co-activation predictor in K1 (pipeline.py:301-321), decode only
     return StrategyKnobs(
-        use_predictor=strategy.kind == "fate", policy=pol.kind, percentile_q=pol.percentile_q, budget_n=n,
+        use_predictor=strategy.kind in ("fate", "eap"), policy="eap" if strategy.kind == "eap" else pol.kind,
+        percentile_q=pol.percentile_q, budget_n=n,
         cached_bits=plan.cached_bits, prefetch_bits=strategy.prefetch_bits(), ondemand_bits=strategy.ondemand_bits(),
         prefill_use_predictor=strategy.kind == "fate", reorder_prefill=strategy.reorder_prefill,
         p_int2=qp.p_int2 if qp else 0.0, prefill_ondemand_bits=strategy.ondemand_bits() if strategy.kind == "fate" else 16)
@@ -298,7 +298,7 @@ def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timi
         raise TraceMismatch(f"prefill simulation given a {trace.phase} trace")
     validate_trace_for(trace, cfg)
     if eap_stats is not None or strategy.kind == "eap":
-        raise InvalidConfig("the EAP baseline is not implemented on the B200 engine (SURVEY.md §8f rank 2)")
+        raise InvalidConfig("the EAP baseline runs decode only on the B200 engine; EAP prefill is not implemented")
     _check_weights(weights, cfg)
     n = transfer_budget(timing, strategy.prefetch_bits()) if strategy.prefetch_bits() in timing.t_expert_io else 0
     knobs = knobs_for(strategy, plan, n)

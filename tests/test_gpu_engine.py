@@ -86,6 +86,50 @@ def test_decode_n0_and_topk_variants():
         eng.close()
 
 
+@pytest.mark.parametrize("name", ["tiny", "qwen"])
+def test_decode_eap_baseline(name):
+    """EAP baseline (pipeline.py:301-321) in K1: co-activation observe + scored
+    top-k prediction, 16-bit prefetch / on-demand, against the oracle and the
+    reference's own EAP log."""
+    e = golden()["schedules"][name]
+    want = e["decode_eap"]
+    kw = {"policy": "eap", "prefetch_bits": 16, "ondemand_bits": 16, "cached_bits": 4,
+          "prefill_use_predictor": False}
+    cfg, dec, pre, w, store, eng = _engine(name, n=want["n"], knobs_kw=kw, bits=(16, 4))
+    gd, chd, g, ch = _dev_trace(dec, cfg)
+    res = eng.decode(gd, chd, want_logs=True)
+    oracle = O.decode_schedule(g, ch.tolist(), np.stack(w.matrices), np.array(w.temperatures), e["plan"],
+                               cfg.top_k, want["n"], O.StrategyKnobs(kind="eap", quant=False, policy_kind="topk"), 4)
+    _compare_steps(res.logs, oracle)
+    _compare_steps(res.logs, want)
+    for l in range(cfg.num_layers):
+        assert eng.arc_state(l) == want["arcs"][l]
+    st = res.stats
+    assert st["dequant_count"] == want["report"]["dequant_count"]
+    assert st["recall_sum"] / st["recall_n"] == pytest.approx(want["report"]["recall"], abs=1e-12)
+    assert st["prefetch_issued"] == want["transfers"]["prefetch"]
+    assert st["ondemand_issued"] == want["transfers"]["ondemand"]
+    eng.close()
+
+
+def test_simulate_decoding_eap_public_api():
+    """The drop-in call a moesim user makes: pipeline.simulate_decoding with
+    Strategy.eap() reproduces the reference's timing-independent report fields."""
+    from golden_util import PAPER_TIMING
+    from paper_2502_12224_b200 import cache, core, pipeline
+    e = golden()["schedules"]["tiny"]
+    want = e["decode_eap"]["report"]
+    cfg, dec, pre, w = config_traces("tiny")
+    budget = cfg.dense_bytes + 12 * cfg.expert_bytes[4]
+    plan = cache.plan_allocation(cfg, budget, 4)
+    assert list(plan.per_layer_capacity) == e["plan"]
+    tl, rep = pipeline.simulate_decoding(dec, pipeline.Strategy.eap(), plan, core.TimingModel(**PAPER_TIMING), cfg,
+                                         weights=w)
+    assert rep.strategy == "eap"
+    assert rep.dequant_count == want["dequant_count"]
+    assert rep.recall == pytest.approx(want["recall"], abs=1e-12)
+
+
 def test_decode_outputs_match_fp64_oracle():
     """y[t, l] = sum_e w_e FFN_e(sqrt(H) * gate_in) with each expert dequantized
     from the copy the GPU actually used (src_bits), plus the shared expert."""

@@ -130,8 +130,10 @@ def test_strategy_and_budget():
     assert pipeline.transfer_budget(tm, 4) == 4
     knobs = pipeline.knobs_for(s, cache.plan_allocation(_cfg(), 12 * 245760, 4), 4)
     assert (knobs.use_predictor, knobs.policy, knobs.budget_n, knobs.prefill_ondemand_bits) == (True, "percentile", 4, 2)
-    with pytest.raises(errors.InvalidConfig):
-        pipeline.knobs_for(pipeline.Strategy.eap(), cache.zero_plan(_cfg()), 0)
+    # EAP maps onto the engine's co-activation predictor (policy "eap"), 16-bit transfers, decode only
+    ek = pipeline.knobs_for(pipeline.Strategy.eap(), cache.zero_plan(_cfg()), 3)
+    assert (ek.use_predictor, ek.policy, ek.budget_n, ek.prefetch_bits, ek.ondemand_bits,
+            ek.prefill_use_predictor) == (True, "eap", 3, 16, 16, False)
 
 
 def test_unbound_cache_protocol():
