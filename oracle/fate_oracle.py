@@ -347,7 +347,8 @@ def eap_list(counts_l: np.ndarray, chosen, k: int) -> list[int]:
 
 
 def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
-                    knobs: StrategyKnobs, cached_bits: int, arcs: list | None = None) -> dict:
+                    knobs: StrategyKnobs, cached_bits: int, arcs: list | None = None,
+                    eap_counts: np.ndarray | None = None) -> dict:
     """Timing-independent fields of simulate_decoding (pipeline.py:343-517).
 
     gate_in [T, L, H] fp64, chosen [T][L] ids.  Per (token, layer) step:
@@ -366,7 +367,8 @@ def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
     use_pred = knobs.kind == "fate"
     use_eap = knobs.kind == "eap"
     E = int(np.asarray(mats).shape[1])
-    counts = np.zeros((max(L - 1, 1), E, E), dtype=np.int64)  # EapStats (predict.py:110-130)
+    # EapStats (predict.py:110-130); shared with a preceding prefill when chained
+    counts = eap_counts if eap_counts is not None else np.zeros((max(L - 1, 1), E, E), dtype=np.int64)
     for t in range(T):
         for l in range(L):
             rec = {"token": t, "layer": l}
@@ -424,7 +426,8 @@ def decode_schedule(gate_in, chosen, mats, taus, caps, k: int, budget_n: int,
 
 
 def prefill_schedule(gate_in, chosen, mats, taus, caps, k: int, knobs: StrategyKnobs,
-                     cached_bits: int, started: dict | None = None, arcs: list | None = None) -> dict:
+                     cached_bits: int, started: dict | None = None, arcs: list | None = None,
+                     eap_counts: np.ndarray | None = None) -> dict:
     """Timing-independent fields of simulate_prefill (pipeline.py:536-778).
 
     ``started[layer]`` is the set of that layer's prefetches that had begun
@@ -438,13 +441,28 @@ def prefill_schedule(gate_in, chosen, mats, taus, caps, k: int, knobs: StrategyK
     profiles: dict = {}
     layers = []
     recall_sum, recall_n, dequant = 0.0, 0, 0
+    if knobs.kind == "eap" and eap_counts is None:
+        E = int(np.asarray(mats).shape[1])
+        eap_counts = np.zeros((max(L - 1, 1), E, E), dtype=np.int64)
     for l in range(L):
         rec = {"layer": l}
-        if knobs.kind == "fate" and l + 1 < L:
+        lists = None
+        if knobs.kind == "eap":
+            # EAP prefill (pipeline.py:652-665): every token's transition l-1 -> l
+            # first (eap_update), then per-token EAP lists for l+1 (merged_topk_lists)
+            if l > 0:
+                for t in range(T):
+                    nxt = sorted(int(x) for x in chosen[t][l])
+                    for a in sorted(int(x) for x in chosen[t][l - 1]):
+                        eap_counts[l - 1, a, nxt] += 1
+            if l + 1 < L:
+                lists = [eap_list(eap_counts[l], chosen[t][l], k) for t in range(T)]
+        elif knobs.kind == "fate" and l + 1 < L:
             lists = []
             for t in range(T):
                 w = gate_routing(mats[l + 1], taus[l + 1], gate_in[t][l])
                 lists.append(top_k(w, k))
+        if lists is not None:
             counts, order = popularity(lists)
             bits = assign_bits_prefill(order, knobs.p_int2) if knobs.quant else {e: 16 for e in order}
             if not knobs.reorder_prefill:

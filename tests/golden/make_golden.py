@@ -144,13 +144,13 @@ def report_dict(rep):
                                          "recall", "hit_rate", "stall_ms", "dequant_count")}
 
 
-def run_decode_logged(trace, strategy, plan, timing, cfg, weights, cache):
+def run_decode_logged(trace, strategy, plan, timing, cfg, weights, cache, eap_stats=None):
     LOG.clear()
     mpipe._Channel = LogChannel
     if strategy.kind == "fate":
         pred = LogPredictor(weights, strategy.prefetch_policy, cfg.top_k)
     elif strategy.kind == "eap":
-        pred = LogEapPredictor(cfg.num_layers, cfg.num_experts, cfg.top_k)
+        pred = LogEapPredictor(cfg.num_layers, cfg.num_experts, cfg.top_k, stats=eap_stats)
     else:
         pred = None
     tl, rep = mpipe.simulate_decoding(trace, strategy, plan, timing, cfg, weights=weights, cache=cache,
@@ -186,10 +186,11 @@ def run_decode_logged(trace, strategy, plan, timing, cfg, weights, cache):
                           "ondemand": sum(1 for x in enq if x[0] == "ondemand")}}
 
 
-def run_prefill_logged(trace, strategy, plan, timing, cfg, weights, cache):
+def run_prefill_logged(trace, strategy, plan, timing, cfg, weights, cache, eap_stats=None):
     LOG.clear()
     mpipe._Channel = LogChannel
-    tl, rep = mpipe.simulate_prefill(trace, strategy, plan, timing, cfg, weights=weights, cache=cache)
+    tl, rep = mpipe.simulate_prefill(trace, strategy, plan, timing, cfg, weights=weights, cache=cache,
+                                     eap_stats=eap_stats)
     enq = LOG.get("enqueue", [])
     dropped = LOG.get("dropped", [])
     layers = []
@@ -232,6 +233,13 @@ def eap_entries(sched):
         plan = mcache.plan_allocation(cfg, budget, 4)
         cache = LogCache(plan)
         sched[name]["decode_eap"] = run_decode_logged(dec, mpipe.Strategy.eap(), plan, timing, cfg, w, cache)
+        # compare_strategies chaining (pipeline.py:828-849): prefill then decode share one EapStats
+        cache = LogCache(plan)
+        stats = mpred.EapStats(num_layers=cfg.num_layers, num_experts=cfg.num_experts)
+        sched[name]["prefill_eap"] = run_prefill_logged(pre, mpipe.Strategy.eap(), plan, timing, cfg, w, cache,
+                                                        eap_stats=stats)
+        sched[name]["decode_eap_warm"] = run_decode_logged(dec, mpipe.Strategy.eap(), plan, timing, cfg, w, cache,
+                                                           eap_stats=stats)
 
 
 def main():

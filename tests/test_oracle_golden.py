@@ -152,6 +152,33 @@ def test_prefill_then_decode_schedule(name):
     _check_decode(got, wd)
 
 
+@pytest.mark.parametrize("name", ["tiny", "qwen"])
+def test_eap_prefill_then_decode_schedule(name):
+    """EAP chaining (pipeline.py:828-849): prefill and decode share one EapStats."""
+    e = golden()["schedules"][name]
+    cfg, dec, pre, w = config_traces(name)
+    mats, taus = np.stack(w.matrices), np.array(w.temperatures)
+    arcs = [O.Arc(c) for c in e["plan"]]
+    kn = _knobs(kind="eap", quant=False, policy_kind="topk", reorder_prefill=False)
+    counts = np.zeros((cfg.num_layers - 1, cfg.num_experts, cfg.num_experts), dtype=np.int64)
+    want = e["prefill_eap"]
+    started = {l: set(x["started"]) for l, x in enumerate(want["layers"])}
+    gp, chp = _arrays(pre, cfg)
+    got = O.prefill_schedule(gp, chp, mats, taus, e["plan"], cfg.top_k, kn, 4, started=started, arcs=arcs,
+                             eap_counts=counts)
+    for g, wl in zip(got["layers"], want["layers"]):
+        assert [list(x) for x in g.get("prefetch", [])] == wl["prefetch_for_next"], g["layer"]
+        assert [[x, 16] for x in g["ondemand"]] == wl["ondemand"], g["layer"]
+        assert g["victims"] == wl["victims"], g["layer"]
+    assert got["arcs"] == want["arcs"]
+    assert got["recall"] == pytest.approx(want["report"]["recall"], abs=1e-12)
+    assert got["dequant_count"] == want["report"]["dequant_count"]
+    gd, chd = _arrays(dec, cfg)
+    wd = e["decode_eap_warm"]
+    got = O.decode_schedule(gd, chd, mats, taus, e["plan"], cfg.top_k, wd["n"], kn, 4, arcs=arcs, eap_counts=counts)
+    _check_decode(got, wd)
+
+
 @pytest.mark.parametrize("name", ["qwen", "dsk", "mixtral"])
 def test_decode_schedule_model_shapes(name):
     e = golden()["schedules"][name]
