@@ -170,6 +170,10 @@ int fate_engine_timeline(fate_engine *eng, double *step_ms, int max_steps, doubl
 
 /* Router weights W[L,E,H] fp64 and temperatures tau[L] (host arrays; copied). */
 int fate_engine_set_gate(fate_engine *eng, const double *W_host, const double *tau_host);
+/* EAP baseline (policy 2): co-activation statistics back to empty, i.e. a fresh
+ * EapStats (predict.py:110-130).  Replaces constructing EapDecodePredictor /
+ * EapStats (pipeline.py:301-336, 572-574); prefill and decode otherwise share them. */
+int fate_engine_reset_eap(fate_engine *eng);
 /* Register the pinned host pool for one bit width: experts (l,e) at
  * base + (l*E + e) * stride, each a packed buffer (header + payload). */
 int fate_engine_set_host_pool(fate_engine *eng, int bits, const uint8_t *base_host, int64_t stride);

@@ -97,6 +97,7 @@ SIGNATURES = {
     "fate_engine_set_strategy": (c_int, [c_vp, C.POINTER(EngineConfig)]),
     "fate_engine_timeline": (c_int, [c_vp, c_vp, c_int, c_vp, c_vp, c_int, P_i32]),
     "fate_engine_set_gate": (c_int, [c_vp, c_vp, c_vp]),
+    "fate_engine_reset_eap": (c_int, [c_vp]),
     "fate_engine_set_host_pool": (c_int, [c_vp, c_int, c_vp, c_i64]),
     "fate_engine_set_shared": (c_int, [c_vp, c_int, c_vp]),
     "fate_engine_reset_cache": (c_int, [c_vp]),

@@ -974,6 +974,21 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   return FATE_OK;
 }
 
+// EAP co-activation statistics back to empty (a fresh EapStats, predict.py:110-130).
+// The Python layer calls it for every fresh simulate_prefill / simulate_decoding
+// with Strategy.eap(); compare_strategies keeps them from prefill into decode.
+extern "C" int fate_engine_reset_eap(fate_engine *g) {
+  if (!g) {
+    fate::set_error("fate_engine_reset_eap: null engine");
+    return FATE_EINVAL;
+  }
+  if (cudaMemsetAsync(g->d.eap_counts, 0, g->eap_bytes, g->cstream) != cudaSuccess) {
+    fate::set_error("fate_engine_reset_eap: memset failed");
+    return FATE_ECUDA;
+  }
+  return FATE_OK;
+}
+
 extern "C" int fate_engine_set_gate(fate_engine *g, const double *W_host, const double *tau_host) {
   const size_t n = (size_t)g->cfg.num_layers * g->cfg.num_experts * g->cfg.hidden_dim;
   FATE_CUDA(cudaMemcpy((void *)g->d.W, W_host, n * 8, cudaMemcpyHostToDevice));
@@ -1312,8 +1327,6 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   *g->copy_done_host2 = 0;
   for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
   const cudaStream_t cs = g->cstream;
-  // EAP statistics start empty for every decode call (build_decode_predictor, pipeline.py:324-336)
-  if (g->cfg.use_predictor && g->cfg.policy == 2) FATE_CUDA(cudaMemsetAsync(g->d.eap_counts, 0, g->eap_bytes, cs));
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
   run_begin_kernel<<<1, 1, 0, cs>>>(g->d);
   FATE_CHECK_LAUNCH("run_begin_kernel");
@@ -1653,6 +1666,62 @@ __device__ void sort_by_count_desc(int32_t *ids, const int32_t *cnt, int n) {
   }
 }
 
+// EAP prefill (pipeline.py:652-665), one thread per token, between layer l's
+// gate and the plan kernel: record the token's transition l-1 -> l into the
+// co-activation counts (eap_update; s.chosen still holds layer l-1), then
+// write its EAP list for l+1 (eap_predict predict.py:141-158; top-k by
+// (-score, id), cold start 0..k-1) into s.order_n for prefill_merge.
+__global__ void eap_prefill_kernel(EngineDev d, PfScratch s, int layer, int T, int predict) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int E = d.E, k = d.k;
+  int32_t cur[KMAX];
+  for (int j = 0; j < k; ++j) cur[j] = s.order[(int64_t)t * E + j];
+  for (int i = 1; i < k; ++i)
+    for (int j = i; j > 0 && cur[j - 1] > cur[j]; --j) {
+      const int x = cur[j];
+      cur[j] = cur[j - 1];
+      cur[j - 1] = x;
+    }
+  if (layer > 0) {
+    int32_t *cnt = d.eap_counts + (int64_t)(layer - 1) * E * E;
+    for (int i = 0; i < k; ++i) {
+      const int a = s.chosen[t * k + i];
+      for (int j = 0; j < k; ++j) atomicAdd(&cnt[a * E + cur[j]], 1);
+      atomicAdd(&d.eap_totals[(layer - 1) * E + a], k);
+    }
+  }
+  if (!predict) return;
+  const int32_t *cnt = d.eap_counts + (int64_t)layer * E * E;
+  const int32_t *tot = d.eap_totals + (int64_t)layer * E;
+  int warm = 0;
+  for (int j = 0; j < k; ++j) warm |= tot[cur[j]] != 0;
+  int32_t *out = s.order_n + (int64_t)t * E;
+  if (!warm) {
+    for (int j = 0; j < k; ++j) out[j] = j;
+    return;
+  }
+  double best[KMAX];
+  int32_t bid[KMAX];
+  int nb = 0;
+  for (int e = 0; e < E; ++e) {
+    double sc = 0.0;
+    for (int j = 0; j < k; ++j) {
+      const int a = cur[j];
+      sc = __dadd_rn(sc, __ddiv_rn((double)cnt[a * E + e] + 1.0, (double)(tot[a] + E)));
+    }
+    // insert into the running top-k (ids ascend, so an equal score keeps the lower id first)
+    int pos = nb;
+    while (pos > 0 && sc > best[pos - 1]) --pos;
+    if (pos >= k) continue;
+    for (int i = (nb < k ? nb : k - 1); i > pos; --i) best[i] = best[i - 1], bid[i] = bid[i - 1];
+    best[pos] = sc;
+    bid[pos] = e;
+    if (nb < k) ++nb;
+  }
+  for (int j = 0; j < k; ++j) out[j] = bid[j];
+}
+
 __global__ void __launch_bounds__(1024) prefill_plan_kernel(EngineDev d, PfScratch s, int layer, int T, int predict,
                                                             int reorder, double p_int2, int od_bits,
                                                             const int32_t *__restrict__ trace_chosen,
@@ -1796,6 +1865,16 @@ __global__ void __launch_bounds__(1024) prefill_plan_kernel(EngineDev d, PfScrat
         if (unpl && !mark[e]) mark[e] = 1, fill[nfs++] = e;
       }
     for (int i = 0; i < n_unpl; ++i) od_order[i] = fill[i];
+    for (int e = 0; e < E; ++e) mark[e] = 0, fill[e] = 0;
+    // first-seen rank of every active expert: the host orders the on-demand
+    // loads, prefetches converted at block end included, by it
+    int r = 0;
+    for (int t = 0; t < T && r < n_act; ++t)
+      for (int j = 0; j < k; ++j) {
+        const int e = s.chosen[t * k + j];
+        if (!mark[e]) mark[e] = 1, fill[e] = r++;
+      }
+    for (int i = 0; i < n_act; ++i) msg->active_fs[i] = fill[s.actives[i]];
     for (int e = 0; e < E; ++e) mark[e] = 0, fill[e] = 0;
   }
   for (int i = 0; i < n_unpl; ++i) {
@@ -2033,7 +2112,12 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
     FATE_CUDA(launch_gate_batch(g->d.W + (int64_t)l * E * H, tau[l], gate_in_dev + (int64_t)l * H, (int64_t)L * H, T,
                                 E, H, s.routing, s.order, nullptr, k, 0, 0.5, cs));
     const int pred_here = predict && l + 1 < L;
-    if (pred_here)
+    const bool eap = g->cfg.use_predictor && g->cfg.policy == 2;
+    if (eap && (l > 0 || pred_here)) {
+      eap_prefill_kernel<<<(T + 127) / 128, 128, 0, cs>>>(d, s, l, T, pred_here);
+      FATE_CHECK_LAUNCH("eap_prefill_kernel");
+    }
+    if (pred_here && !eap)
       FATE_CUDA(launch_gate_batch(g->d.W + (int64_t)(l + 1) * E * H, tau[l + 1], gate_in_dev + (int64_t)l * H,
                                   (int64_t)L * H, T, E, H, nullptr, s.order_n, nullptr, k, 0, 0.5, cs));
     prefill_plan_kernel<<<1, 1024, 0, cs>>>(d, s, l, T, pred_here, g->cfg.reorder_prefill, g->cfg.p_int2, od_bits,
@@ -2099,11 +2183,18 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
     }
     std::vector<int> idx(od.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
-    if (g->cfg.reorder_prefill)
+    if (g->cfg.reorder_prefill) {
       std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
         const int ea = od[a].first, eb = od[b].first;
         return cnt[ea] != cnt[eb] ? cnt[ea] > cnt[eb] : ea < eb;
       });
+    } else {
+      // token-request (first-seen) order over every unplanned expert, converted
+      // prefetches included (pipeline.py:701-719 with _first_seen_order :524-533)
+      std::vector<int> rank(E, 1 << 30);
+      for (int i = 0; i < m.n_active; ++i) rank[m.active_e[i]] = m.active_fs[i];
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return rank[od[a].first] < rank[od[b].first]; });
+    }
     // prefetches for l+1 (issued at predict_at, before this layer's on-demand loads)
     for (int i = 0; i < m.n_pf; ++i)
       ch.pending.push_back(Transfer{0, 0, l + 1, m.pf_e[i], m.pf_bits_each[i], m.pf_b[i], m.pf_g[i], -1, -1});

@@ -32,6 +32,7 @@ struct StepMsg {
   // prefill extras (host-side log + ordering)
   int32_t n_active, n_res;
   int32_t active_e[EMAX], active_cnt[EMAX], res_e[EMAX];
+  int32_t active_fs[EMAX];  // prefill, reorder off: first-seen rank of active_e[i] (pipeline.py:524-533)
   int32_t pred_order[EMAX], pred_cnt[EMAX], n_pred;
   int32_t mismatch;
 };

@@ -109,6 +109,10 @@ class OffloadEngine:
     def reset_cache(self) -> None:
         check(self._L.fate_engine_reset_cache(self._h), "fate_engine_reset_cache")
 
+    def reset_eap(self) -> None:
+        """EAP co-activation statistics back to empty (a fresh EapStats, predict.py:110-130)."""
+        check(self._L.fate_engine_reset_eap(self._h), "fate_engine_reset_eap")
+
     def resident(self, layer: int) -> set:
         out = (C.c_int32 * self.cfg.num_experts)()
         check(self._L.fate_engine_resident(self._h, layer, out), "fate_engine_resident")

@@ -152,7 +152,7 @@ def knobs_for(strategy: Strategy, plan: CachePlan, n: int):
         use_predictor=strategy.kind in ("fate", "eap"), policy="eap" if strategy.kind == "eap" else pol.kind,
         percentile_q=pol.percentile_q, budget_n=n,
         cached_bits=plan.cached_bits, prefetch_bits=strategy.prefetch_bits(), ondemand_bits=strategy.ondemand_bits(),
-        prefill_use_predictor=strategy.kind == "fate", reorder_prefill=strategy.reorder_prefill,
+        prefill_use_predictor=strategy.kind in ("fate", "eap"), reorder_prefill=strategy.reorder_prefill,
         p_int2=qp.p_int2 if qp else 0.0, prefill_ondemand_bits=strategy.ondemand_bits() if strategy.kind == "fate" else 16)
 
 
@@ -229,8 +229,12 @@ def _resident_counts(logs, caps, L):
 def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, timing: TimingModel, cfg: ModelConfig,
                       weights=None, cache: LayeredExpertCache | None = None, predictor=None,
                       collect_cache_events: bool = False, *, experts=None, shared_intermediate: int = 0,
-                      return_result: bool = False):
-    """Execute decoding of ``trace`` on the GPU (pipeline.py:343-517 semantics)."""
+                      return_result: bool = False, _eap_continue: bool = False):
+    """Execute decoding of ``trace`` on the GPU (pipeline.py:343-517 semantics).
+
+    Strategy.eap() starts from empty co-activation statistics, as a fresh
+    EapDecodePredictor does; compare_strategies passes ``_eap_continue`` so the
+    decode continues with the statistics its prefill accumulated (pipeline.py:828-849)."""
     import torch
 
     if trace.phase != "decoding":
@@ -246,6 +250,8 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
         experts = default_store(cfg, _bits_needed(strategy, plan), shared_intermediate)
     toks, g, ch = trace.dense_arrays(cfg)
     cache, eng = bind_engine(cache, plan, cfg, weights, experts, knobs, max_tokens=max(len(toks), 1))
+    if strategy.kind == "eap" and not _eap_continue:
+        eng.reset_eap()
     dev = torch.device("cuda", eng.device)
     res = eng.decode(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev), tokens=toks,
                      want_logs=collect_cache_events or return_result == "logs")
@@ -297,8 +303,9 @@ def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timi
     if trace.phase != "prefill":
         raise TraceMismatch(f"prefill simulation given a {trace.phase} trace")
     validate_trace_for(trace, cfg)
-    if eap_stats is not None or strategy.kind == "eap":
-        raise InvalidConfig("the EAP baseline runs decode only on the B200 engine; EAP prefill is not implemented")
+    if eap_stats is not None:
+        raise InvalidConfig("the B200 engine keeps EAP statistics on the device; pass eap_stats=None "
+                            "(compare_strategies shares them between prefill and decode)")
     _check_weights(weights, cfg)
     n = transfer_budget(timing, strategy.prefetch_bits()) if strategy.prefetch_bits() in timing.t_expert_io else 0
     knobs = knobs_for(strategy, plan, n)
@@ -306,6 +313,8 @@ def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timi
         experts = default_store(cfg, _bits_needed(strategy, plan), shared_intermediate)
     toks, g, ch = trace.dense_arrays(cfg)
     cache, eng = bind_engine(cache, plan, cfg, weights, experts, knobs, max_tokens=max(len(toks), 1))
+    if strategy.kind == "eap":
+        eng.reset_eap()  # a fresh EapStats (pipeline.py:572-574)
     dev = torch.device("cuda", eng.device)
     Y, st, logs, step_ms, copies = eng.prefill(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev))
     events = []
@@ -369,7 +378,8 @@ def compare_strategies(cfg: ModelConfig, timing: TimingModel, strategies: Sequen
             if prefill_trace is not None:
                 tl, rep = simulate_prefill(prefill_trace, s, plan, timing, cfg, weights=weights, cache=cache, **kw)
                 rows.append(ComparisonRow(s.kind, "prefill", budget, rep, tl))
-            tl, rep = simulate_decoding(decode_trace, s, plan, timing, cfg, weights=weights, cache=cache, **kw)
+            tl, rep = simulate_decoding(decode_trace, s, plan, timing, cfg, weights=weights, cache=cache,
+                                        _eap_continue=s.kind == "eap" and prefill_trace is not None, **kw)
             rows.append(ComparisonRow(s.kind, "decoding", budget, rep, tl))
     return rows
 

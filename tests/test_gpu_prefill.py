@@ -79,6 +79,56 @@ def test_prefill_then_decode_chain(name):
     eng.close()
 
 
+@pytest.mark.parametrize("name", ["tiny", "qwen"])
+def test_eap_prefill_then_decode_chain(name):
+    """EAP baseline through prefill and the chained decode (pipeline.py:828-849):
+    the co-activation statistics the prefill accumulates on the device carry
+    into the decode; both phases bit-exact against the oracle given the
+    measured started sets, and the decode against the reference's own log
+    when every prefetch had started (as in the reference's timeline)."""
+    import torch
+    from paper_2502_12224_b200.engine import OffloadEngine, StrategyKnobs
+    from paper_2502_12224_b200.experts import ExpertStore
+    e = golden()["schedules"][name]
+    cfg, dec, pre, w = config_traces(name)
+    n = e["decode_eap_warm"]["n"]
+    kn = StrategyKnobs(budget_n=n, policy="eap", prefetch_bits=16, ondemand_bits=16, cached_bits=4,
+                       prefill_ondemand_bits=16, reorder_prefill=False, p_int2=0.0)
+    store = ExpertStore(cfg, bits=(16, 4), seed=0)
+    eng = OffloadEngine(cfg, e["plan"], store, w, kn, max_tokens=max(64, pre.num_tokens))
+    eng.reset_eap()
+    mats, taus = np.stack(w.matrices), np.array(w.temperatures)
+    _, gp, chp = pre.dense_arrays(cfg)
+    Y, st, logs, step_ms, copies = eng.prefill(torch.as_tensor(gp, device="cuda"), torch.as_tensor(chp, device="cuda"))
+    started = {l: set(lg["started"]) for l, lg in enumerate(logs)}
+    arcs = [O.Arc(c) for c in e["plan"]]
+    kno = O.StrategyKnobs(kind="eap", quant=False, policy_kind="topk", reorder_prefill=False)
+    counts = np.zeros((cfg.num_layers - 1, cfg.num_experts, cfg.num_experts), dtype=np.int64)
+    ora = O.prefill_schedule(gp, chp.tolist(), mats, taus, e["plan"], cfg.top_k, kno, 4, started=started, arcs=arcs,
+                             eap_counts=counts)
+    _check_prefill(logs, ora)
+    for l in range(cfg.num_layers):
+        assert eng.arc_state(l) == ora["arcs"][l]
+    assert st["dequant_count"] == ora["dequant_count"]
+    assert st["trace_mismatches"] == 0
+    _, gd, chd = dec.dense_arrays(cfg)
+    res = eng.decode(torch.as_tensor(gd, device="cuda"), torch.as_tensor(chd, device="cuda"), want_logs=True)
+    ord_ = O.decode_schedule(gd, chd.tolist(), mats, taus, e["plan"], cfg.top_k, n, kno, 4, arcs=arcs,
+                             eap_counts=counts)
+    for g, o in zip(res.logs, ord_["steps"]):
+        assert (g["chosen"], g.get("pred"), g.get("prefetch"), g["hits"], g["ondemand"], g["victims"]) == \
+               (o["chosen"], o.get("pred"), o.get("prefetch"), o["hits"], o["ondemand"], o["victims"])
+    for l in range(cfg.num_layers):
+        assert eng.arc_state(l) == ord_["arcs"][l]
+    want_started = {l: set(x["started"]) for l, x in enumerate(e["prefill_eap"]["layers"])}
+    if started == want_started:
+        want = e["decode_eap_warm"]
+        for g, wst in zip(res.logs, want["steps"]):
+            assert (g.get("pred"), g.get("prefetch"), g["hits"], g["ondemand"], g["victims"]) == \
+                   (wst.get("pred"), wst.get("prefetch"), wst["hits"], wst["ondemand"], wst["victims"])
+    eng.close()
+
+
 def test_prefill_outputs_match_fp64_oracle():
     import torch
     cfg, dec, pre, w, store, eng, e = _setup("tiny", shared=512)

@@ -133,7 +133,7 @@ def test_strategy_and_budget():
     # EAP maps onto the engine's co-activation predictor (policy "eap"), 16-bit transfers, decode only
     ek = pipeline.knobs_for(pipeline.Strategy.eap(), cache.zero_plan(_cfg()), 3)
     assert (ek.use_predictor, ek.policy, ek.budget_n, ek.prefetch_bits, ek.ondemand_bits,
-            ek.prefill_use_predictor) == (True, "eap", 3, 16, 16, False)
+            ek.prefill_use_predictor) == (True, "eap", 3, 16, 16, True)
 
 
 def test_unbound_cache_protocol():
