@@ -130,6 +130,25 @@ def test_simulate_decoding_eap_public_api():
     assert rep.recall == pytest.approx(want["recall"], abs=1e-12)
 
 
+def test_compare_strategies_fate_eap_lod():
+    """The reference harness call (pipeline.py:802-851) on the GPU engine: per
+    strategy a prefill on a fresh cache, then decode on the warmed one; EAP's
+    statistics carry from its prefill into its decode.  Recall is timing-
+    independent, so it must equal the reference's chained decode."""
+    from golden_util import PAPER_TIMING
+    from paper_2502_12224_b200 import core, pipeline
+    e = golden()["schedules"]["tiny"]
+    cfg, dec, pre, w = config_traces("tiny")
+    budget = cfg.dense_bytes + 12 * cfg.expert_bytes[4]
+    strategies = [pipeline.Strategy.fate(), pipeline.Strategy.eap(), pipeline.Strategy.lod()]
+    rows = pipeline.compare_strategies(cfg, core.TimingModel(**PAPER_TIMING), strategies, [budget], pre, dec, weights=w)
+    got = {(r.strategy, r.phase): r.report for r in rows}
+    assert set(got) == {(k, ph) for k in ("fate", "eap", "lod") for ph in ("prefill", "decoding")}
+    assert got[("fate", "decoding")].recall == pytest.approx(e["decode_warm"]["report"]["recall"], abs=1e-12)
+    assert got[("eap", "decoding")].recall == pytest.approx(e["decode_eap_warm"]["report"]["recall"], abs=1e-12)
+    assert got[("lod", "decoding")].recall == 0.0
+
+
 def test_decode_outputs_match_fp64_oracle():
     """y[t, l] = sum_e w_e FFN_e(sqrt(H) * gate_in) with each expert dequantized
     from the copy the GPU actually used (src_bits), plus the shared expert."""
