@@ -6,7 +6,8 @@
 //
 // The op is a chain of GEMVs: pure HBM streaming, and the B200 design is a
 // TMA-bulk pipeline per SM:
-//  * one persistent CTA per SM: warp 0 is the producer, warps 1..16 consume;
+//  * one persistent CTA per SM: warps 0-3 produce (tile g of the stage
+//    sequence on warp g mod 4), warps 4-15 consume;
 //  * weights move global -> shared with cp.async.bulk (the TMA engine; SASS
 //    UBLKCP) into a ring of 32 KB stages completed on mbarriers, so ~100 KB
 //    per SM are in flight independently of register pressure, and every
@@ -495,17 +496,17 @@ __device__ __forceinline__ void down_tile_bits(const TileMeta &tm, const uint8_t
 
 // One launch per decode step:
 //   phase A  gate+up rows: a = silu(W1 x) * (W3 x).  Tiles go round-robin
-//            over the CTAs; warp w takes the rows of tile k whose running index
-//            is w mod 16, so the rows of consecutive tiles land on different
-//            warps; a goes straight into the chunk-transposed layout of its
+//            over the CTAs; consumer warp w takes the rows of tile k whose
+//            running index is w mod 12, so the rows of consecutive tiles land
+//            on different warps; a goes straight into the chunk-transposed layout of its
 //            expert (alay, global);
 //   barrier  grid-wide (all CTAs resident) so every activation is visible;
 //   phase B  each CTA owns a block of output rows (sub-blocks of <= 16) and
 //            streams column ranges of those rows of W2 of every expert; the
-//            16 consumer warps split the columns (chunk groups) and rows
+//            12 consumer warps split the columns (chunk groups) and rows
 //            (r = 4m + w%4), accumulating w_j * dot in registers across all
 //            tiles, then one fixed-order reduction per row: y is deterministic.
-// The producer never waits for the barrier: W2 tiles are in flight while
+// The producers never wait for the barrier: W2 tiles are in flight while
 // phase A drains.
 template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
