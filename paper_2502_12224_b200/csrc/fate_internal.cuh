@@ -138,7 +138,15 @@ __device__ inline void write_xlay(const float *x, int H, float4 *xlay, int tid, 
     float *sums = reinterpret_cast<float *>(xt + H / 4);
     for (int i = tid; i < H / 4; i += nthr) {
       const int c = (4 * i) / cols, m = ((4 * i) % cols) / 4;
-      xt[m * nch + c] = reinterpret_cast<const float4 *>(x)[i];
+      float4 v = reinterpret_cast<const float4 *>(x)[i];
+      if (sl == 2) {
+        // INT4 width: element 4m+j prescaled by 2^-4j (exact), so K3 reads nibble j of
+        // each 16-bit half in place as c * 2^4j (see word_dot<4>); the sums stay unscaled
+        v.y *= 0.0625f;
+        v.z *= 0.00390625f;
+        v.w *= 0.000244140625f;
+      }
+      xt[m * nch + c] = v;
     }
     for (int c = tid; c < nch; c += nthr) {
       float acc = 0.f;

@@ -91,10 +91,20 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the con
 // float is 2^23 + byte exactly; one FSUB2 removes the offset for two codes.
 
 constexpr uint32_t kMagic23 = 0x4B000000u;
+__constant__ float kInt4Prescale[4] = {1.0f, 0.0625f, 0.00390625f, 0.000244140625f};
 
 template <int K>
 __device__ __forceinline__ float mag(uint32_t v) {
   return __uint_as_float(__byte_perm(v, kMagic23, 0x7650 + K));
+}
+
+// nibble J of v kept in place under the 2^23 magic: 2^23 + c * 2^4J (one LOP3; the magic
+// comes in a register so the AND and the OR fuse)
+template <int J>
+__device__ __forceinline__ float nib(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(v), "n"(0xFu << (4 * J)), "r"(kMagic23));
+  return __uint_as_float(r);
 }
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -128,6 +138,10 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ float2 lo2(const float4 &v) { return make_float2(v.x, v.y); }
+// (x0 + x2, x1 + x3) of a prescaled INT4 activation quad, exactly as from the unscaled one
+__device__ __forceinline__ float2 unscale4(const float4 &v) {
+  return ffma2(make_float2(v.z, v.w), make_float2(256.0f, 4096.0f), make_float2(v.x, 16.0f * v.y));
+}
 __device__ __forceinline__ float2 hi2(const float4 &v) { return make_float2(v.z, v.w); }
 
 template <int WI>
@@ -144,12 +158,15 @@ __device__ __forceinline__ void word_dot(uint32_t w, const float4 (&xv)[4], floa
     a0 = ffma2(fsub2(make_float2(mag<0>(w), mag<1>(w)), m), lo2(xv[0]), a0);
     a1 = ffma2(fsub2(make_float2(mag<2>(w), mag<3>(w)), m), hi2(xv[0]), a1);
   } else if constexpr (BITS == 4) {
-    // elements 2k | 2k+1 in byte k; the shift runs on the FMA pipe (IMAD.HI), the ALU pipe is the bound
-    const uint32_t lo = w & 0x0F0F0F0Fu, hi = __umulhi(w, 1u << 28) & 0x0F0F0F0Fu;
-    a0 = ffma2(fsub2(make_float2(mag<0>(lo), mag<0>(hi)), m), lo2(xv[0]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<1>(lo), mag<1>(hi)), m), hi2(xv[0]), a1);
-    a0 = ffma2(fsub2(make_float2(mag<2>(lo), mag<2>(hi)), m), lo2(xv[1]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<3>(lo), mag<3>(hi)), m), hi2(xv[1]), a1);
+    // element p of the word is nibble p.  Nibbles 0-3 of w and of w >> 16 (IMAD.HI, FMA
+    // pipe) are masked in place under the 2^23 magic: one LOP3 each gives 2^23 + c * 2^4j
+    // exactly (j = p mod 4); the x layout is prescaled by 2^-4j, so every product is c * x
+    // rounded as before.  8 ALU ops per word instead of 2 LOP3 + 8 PRMT.
+    const uint32_t hw = __umulhi(w, 1u << 16);
+    a0 = ffma2(fsub2(make_float2(nib<0>(w), nib<1>(w)), m), lo2(xv[0]), a0);
+    a1 = ffma2(fsub2(make_float2(nib<2>(w), nib<3>(w)), m), hi2(xv[0]), a1);
+    a0 = ffma2(fsub2(make_float2(nib<0>(hw), nib<1>(hw)), m), lo2(xv[1]), a0);
+    a1 = ffma2(fsub2(make_float2(nib<2>(hw), nib<3>(hw)), m), hi2(xv[1]), a1);
   } else {
     static_assert(BITS == 2, "2/4/8-bit codes");
     const uint32_t b0 = w & 0x03030303u, b1 = (w >> 2) & 0x03030303u;  // elements 4k+s in byte k of b_s
@@ -414,7 +431,7 @@ __device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, 
   if constexpr ((WI) < U) {                                                \
     _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                   \
       xv[qi] = at[((h * U + (WI)) * qpw + qi) * nchI + cg];                \
-      sa = fadd2(sa, fadd2(lo2(xv[qi]), hi2(xv[qi])));                     \
+      sa = fadd2(sa, BITS == 4 ? unscale4(xv[qi]) : fadd2(lo2(xv[qi]), hi2(xv[qi]))); \
     }                                                                      \
     _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]); \
   }
@@ -745,7 +762,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       if (lane == 0) {
         // straight into the chunk-transposed activation layout of phase B
         const int r = r0 + row, c = r >> lc, m = (r & ((1 << lc) - 1)) >> 2;
-        aj[(m * nch_a + c) * 4 + (r & 3)] = u / (1.0f + expf(-u)) * v;
+        float a = u / (1.0f + expf(-u)) * v;
+        if (bits == 4) a *= kInt4Prescale[r & 3];  // the INT4 activation layout is prescaled like x
+        aj[(m * nch_a + c) * 4 + (r & 3)] = a;
       }
       if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 8) {
         g_k3_sub[k][0] = c0;
