@@ -145,6 +145,13 @@ __device__ inline void write_xlay(const float *x, int H, float4 *xlay, int tid, 
         v.y *= 0.0625f;
         v.z *= 0.00390625f;
         v.w *= 0.000244140625f;
+      } else if (sl == 3) {
+        // INT2 width: element e prescaled by 4^-(e mod 8) (word_dot<2>)
+        const float b = (m & 1) ? 0.00390625f : 1.0f;  // 4^-4 for odd quads
+        v.x *= b;
+        v.y *= b * 0.25f;
+        v.z *= b * 0.0625f;
+        v.w *= b * 0.015625f;
       }
       xt[m * nch + c] = v;
     }

@@ -92,6 +92,8 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the con
 
 constexpr uint32_t kMagic23 = 0x4B000000u;
 __constant__ float kInt4Prescale[4] = {1.0f, 0.0625f, 0.00390625f, 0.000244140625f};
+__constant__ float kInt2Prescale[8] = {1.0f, 0.25f, 0.0625f, 0.015625f, 0.00390625f, 0.0009765625f, 0.000244140625f,
+                                       6.103515625e-05f};
 
 template <int K>
 __device__ __forceinline__ float mag(uint32_t v) {
@@ -104,6 +106,14 @@ template <int J>
 __device__ __forceinline__ float nib(uint32_t v) {
   uint32_t r;
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(v), "n"(0xFu << (4 * J)), "r"(kMagic23));
+  return __uint_as_float(r);
+}
+
+// 2-bit field J of v in place under the 2^23 magic: 2^23 + c * 4^J (one LOP3)
+template <int J>
+__device__ __forceinline__ float crumb(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(v), "n"(0x3u << (2 * J)), "r"(kMagic23));
   return __uint_as_float(r);
 }
 
@@ -138,6 +148,11 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ float2 lo2(const float4 &v) { return make_float2(v.x, v.y); }
+// (x0 + x2, x1 + x3) of a prescaled INT2 activation quad (odd quads carry another 4^-4)
+__device__ __forceinline__ float2 unscale2(const float4 &v, int odd) {
+  const float b = odd ? 256.0f : 1.0f;
+  return ffma2(make_float2(v.z, v.w), make_float2(16.0f * b, 64.0f * b), make_float2(v.x * b, 4.0f * b * v.y));
+}
 // (x0 + x2, x1 + x3) of a prescaled INT4 activation quad, exactly as from the unscaled one
 __device__ __forceinline__ float2 unscale4(const float4 &v) {
   return ffma2(make_float2(v.z, v.w), make_float2(256.0f, 4096.0f), make_float2(v.x, 16.0f * v.y));
@@ -169,16 +184,17 @@ __device__ __forceinline__ void word_dot(uint32_t w, const float4 (&xv)[4], floa
     a1 = ffma2(fsub2(make_float2(nib<2>(hw), nib<3>(hw)), m), hi2(xv[1]), a1);
   } else {
     static_assert(BITS == 2, "2/4/8-bit codes");
-    const uint32_t b0 = w & 0x03030303u, b1 = (w >> 2) & 0x03030303u;  // elements 4k+s in byte k of b_s
-    const uint32_t b2 = (w >> 4) & 0x03030303u, b3 = (w >> 6) & 0x03030303u;
-    a0 = ffma2(fsub2(make_float2(mag<0>(b0), mag<0>(b1)), m), lo2(xv[0]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<0>(b2), mag<0>(b3)), m), hi2(xv[0]), a1);
-    a0 = ffma2(fsub2(make_float2(mag<1>(b0), mag<1>(b1)), m), lo2(xv[1]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<1>(b2), mag<1>(b3)), m), hi2(xv[1]), a1);
-    a0 = ffma2(fsub2(make_float2(mag<2>(b0), mag<2>(b1)), m), lo2(xv[2]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<2>(b2), mag<2>(b3)), m), hi2(xv[2]), a1);
-    a0 = ffma2(fsub2(make_float2(mag<3>(b0), mag<3>(b1)), m), lo2(xv[3]), a0);
-    a1 = ffma2(fsub2(make_float2(mag<3>(b2), mag<3>(b3)), m), hi2(xv[3]), a1);
+    // element p = 2-bit field p; fields 0-7 of w and of w >> 16 masked in place
+    // (2^23 + c * 4^q exactly, q = p mod 8) against x prescaled by 4^-q
+    const uint32_t hw = __umulhi(w, 1u << 16);
+    a0 = ffma2(fsub2(make_float2(crumb<0>(w), crumb<1>(w)), m), lo2(xv[0]), a0);
+    a1 = ffma2(fsub2(make_float2(crumb<2>(w), crumb<3>(w)), m), hi2(xv[0]), a1);
+    a0 = ffma2(fsub2(make_float2(crumb<4>(w), crumb<5>(w)), m), lo2(xv[1]), a0);
+    a1 = ffma2(fsub2(make_float2(crumb<6>(w), crumb<7>(w)), m), hi2(xv[1]), a1);
+    a0 = ffma2(fsub2(make_float2(crumb<0>(hw), crumb<1>(hw)), m), lo2(xv[2]), a0);
+    a1 = ffma2(fsub2(make_float2(crumb<2>(hw), crumb<3>(hw)), m), hi2(xv[2]), a1);
+    a0 = ffma2(fsub2(make_float2(crumb<4>(hw), crumb<5>(hw)), m), lo2(xv[3]), a0);
+    a1 = ffma2(fsub2(make_float2(crumb<6>(hw), crumb<7>(hw)), m), hi2(xv[3]), a1);
   }
 }
 
@@ -431,7 +447,8 @@ __device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, 
   if constexpr ((WI) < U) {                                                \
     _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                   \
       xv[qi] = at[((h * U + (WI)) * qpw + qi) * nchI + cg];                \
-      sa = fadd2(sa, BITS == 4 ? unscale4(xv[qi]) : fadd2(lo2(xv[qi]), hi2(xv[qi]))); \
+      sa = fadd2(sa, BITS == 4 ? unscale4(xv[qi]) : BITS == 2 ? unscale2(xv[qi], qi & 1)  \
+                                                   : fadd2(lo2(xv[qi]), hi2(xv[qi])));               \
     }                                                                      \
     _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]); \
   }
@@ -763,7 +780,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
         // straight into the chunk-transposed activation layout of phase B
         const int r = r0 + row, c = r >> lc, m = (r & ((1 << lc) - 1)) >> 2;
         float a = u / (1.0f + expf(-u)) * v;
-        if (bits == 4) a *= kInt4Prescale[r & 3];  // the INT4 activation layout is prescaled like x
+        if (bits == 4) a *= kInt4Prescale[r & 3];  // the INT4 / INT2 activation layouts are prescaled like x
+        else if (bits == 2) a *= kInt2Prescale[r & 7];
         aj[(m * nch_a + c) * 4 + (r & 3)] = a;
       }
       if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 8) {
