@@ -99,45 +99,87 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU path (oracle port): fp64 gate + top-k + dequant-fused FFN in C threads
+# CPU path (oracle port, test infrastructure): the whole executed decode path on
+# the host cores -- fp64 gate + top-k, prediction, ARC, and the expert FFN in the
+# width each copy has (AVX2 C threads) -- timed as one (oracle.port_decode)
+
+REF_N = 0  # transfer budget n of the GPU arm on B200 (its measured TimingModel gives 0; the line states it)
 
 
-def cpu_decode(cfg, trace, weights, get_buf, shared_buf, tokens: int, lib) -> float:
-    """Decode `tokens` tokens of the trace on the host; returns seconds."""
+def cpu_port(cfg, trace, weights, plan, n, tokens, get_buf, shared_buf, lib, ffn=True):
+    """Run the CPU restatement on the first `tokens` tokens; returns (seconds, logs)."""
     from oracle import fate_oracle as O
-    _, g, ch = trace.dense_arrays(cfg)
-    H, I, Is = cfg.hidden_dim, cfg.intermediate_dim, QWEN["shared"]
-    scratch = np.empty(cfg.top_k * I + Is, np.float32)
+    _, g, _ = trace.dense_arrays(cfg)
+    mats, taus = np.stack(weights.matrices), np.array(weights.temperatures)
     t0 = time.perf_counter()
-    for t in range(tokens):
-        for l in range(cfg.num_layers):
-            w = O.gate_routing(weights.matrices[l], weights.temperatures[l], g[t, l])
-            chosen = sorted(O.top_k(w, cfg.top_k))
-            x = (np.sqrt(H) * g[t, l]).astype(np.float32)
-            bufs = [get_buf(l, e) for e in chosen] + [shared_buf(l)]
-            O.cpu_ffn(lib, x, bufs, [I] * len(chosen) + [Is], [4] * len(chosen) + [16],
-                      [float(w[e]) for e in chosen] + [1.0], scratch)
-    return time.perf_counter() - t0
+    logs = O.port_decode(g, mats, taus, list(plan.per_layer_capacity), cfg.top_k, n, O.StrategyKnobs(), get_buf,
+                         shared_buf, cfg.hidden_dim, cfg.intermediate_dim, QWEN["shared"], lib, tokens, ffn=ffn)
+    return time.perf_counter() - t0, logs
+
+
+def reference_as_is(cfg, trace, weights, plan_caps, tokens):
+    """The reference simulator itself (moesim.pipeline.simulate_decoding, installed in
+    baseline/_ref) on the same sample trace: policy + discrete-event simulation wall
+    clock with the paper TimingModel (it executes no expert FFN).  None when absent."""
+    import tempfile
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "moesim")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from moesim import cache as mc, core as mcore, gatesim as mg, pipeline as mp
+        from paper_2502_12224_b200 import core
+        from paper_2502_12224_b200.core import GateTrace
+        recs = [r for r in trace.records if r.token_index < tokens]
+        sample = GateTrace(records=tuple(recs), phase=trace.phase, provenance=trace.provenance)
+        with tempfile.TemporaryDirectory() as d:
+            pth = os.path.join(d, "t.ndjson")
+            core.write_trace(sample, pth)
+            mtrace = mcore.read_trace(pth)
+        mcfg = mcore.ModelConfig(num_layers=cfg.num_layers, num_experts=cfg.num_experts, top_k=cfg.top_k,
+                                 hidden_dim=cfg.hidden_dim, shallow_boundary_L=cfg.shallow_boundary_L,
+                                 expert_bytes=dict(cfg.expert_bytes), dense_bytes=cfg.dense_bytes)
+        mw = mg.GateWeights(matrices=[np.asarray(m) for m in weights.matrices],
+                            temperatures=[float(t) for t in weights.temperatures])
+        timing = mcore.TimingModel(t_moe=13.0, t_attn=9.0, t_gate=2.0, t_expert_io={16: 6.0, 8: 3.0, 4: 1.6, 2: 0.85})
+        mplan = mc.plan_allocation(mcfg, cfg.dense_bytes + QWEN["slots"] * cfg.expert_bytes[4], 4)
+        assert list(mplan.per_layer_capacity) == list(plan_caps)
+        t0 = time.perf_counter()
+        mp.simulate_decoding(mtrace, mp.Strategy.fate(), mplan, timing, mcfg, weights=mw)
+        secs = time.perf_counter() - t0
+        return {"value": tokens / secs, "unit": "tokens/s (simulator wall clock)", "cores": 1,
+                "sample": f"moesim.pipeline.simulate_decoding over the first {tokens} tokens of the same trace "
+                          "(reference as is: schedule + discrete-event clock, no expert FFN executed)"}
+    except Exception as e:  # the reference is a baseline, never a reason to fail the bench
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    finally:
+        sys.path.remove(ref)
 
 
 def run_reference(args):
-    """--impl reference: the oracle port on the host cores (rank 0 only)."""
+    """--impl reference: the CPU restatement of the path on the host cores (rank 0 only),
+    on the GPU arm's workload: the same Qwen trace (seed 0), plan and transfer budget,
+    every routed expert in the width the GPU computes it in (INT2 on-demand copies, the
+    slot's width on a hit) and the bf16 shared expert.  Expert codes are random bytes in
+    those formats (the arithmetic does not depend on their values)."""
     from oracle import fate_oracle as O
     from paper_2502_12224_b200 import core
+    from paper_2502_12224_b200.cache import plan_allocation
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = qwen_cfg()
     tokens = args.ref_tokens
-    trace, weights = make_trace(cfg, tokens, 0)
+    trace, weights = make_trace(cfg, args.tokens, 0)
+    plan = plan_allocation(cfg, cfg.dense_bytes + QWEN["slots"] * cfg.expert_bytes[4], 4)
     lib = O.cpu_lib()
     cores = lib.fate_cpu_threads(0)
     rng = np.random.default_rng(0)
     H, I, Is = cfg.hidden_dim, cfg.intermediate_dim, QWEN["shared"]
-    nb4, nb16 = core.packed_expert_bytes(3 * H * I, 4), core.packed_expert_bytes(3 * H * Is, 16)
     bufs: dict = {}
 
-    def rand_buf(nb, I_, bits):
+    def rand_buf(I_, bits):
+        nb = core.packed_expert_bytes(3 * H * I_, bits)
         b = np.frombuffer(rng.bytes(256 + nb), dtype=np.uint8).copy()
         lay = O.buffer_layout(H, I_, bits)
         if bits != 16:  # sane fp32 scale/zero so the FFN does real arithmetic
@@ -147,32 +189,34 @@ def run_reference(args):
             b[256:].view(np.uint16)[:] = 0x3C00
         return b
 
-    # every expert buffer the sample touches is built before the timed steps
-    # (setdefault would evaluate rand_buf on every access and time buffer generation)
-    _, g_s, _ = trace.dense_arrays(cfg)
-    for t in range(tokens):
-        for l in range(cfg.num_layers):
-            w_ = O.gate_routing(weights.matrices[l], weights.temperatures[l], g_s[t, l])
-            for e in O.top_k(w_, cfg.top_k):
-                if (l, e) not in bufs:
-                    bufs[(l, e)] = rand_buf(nb4, I, 4)
+    # every buffer the sample touches is built before the timed steps
+    _, logs = cpu_port(cfg, trace, weights, plan, REF_N, tokens, None, None, lib, ffn=False)
+    for s, lg in enumerate(logs):
+        for e, b in zip(lg["chosen"], lg["fmt_bits"]):
+            if (s % cfg.num_layers, e, b) not in bufs:
+                bufs[(s % cfg.num_layers, e, b)] = rand_buf(I, b)
     for l in range(cfg.num_layers):
-        bufs[("s", l)] = rand_buf(nb16, Is, 16)
-    get_buf = lambda l, e: bufs[(l, e)]  # noqa: E731
+        bufs[("s", l)] = rand_buf(Is, 16)
+    get_buf = lambda l, e, b: bufs[(l, e, b)]  # noqa: E731
     shared = lambda l: bufs[("s", l)]  # noqa: E731
     for _ in range(args.warmup):
-        cpu_decode(cfg, trace, weights, get_buf, shared, tokens, lib)
-    times = [cpu_decode(cfg, trace, weights, get_buf, shared, tokens, lib) for _ in range(args.steps)]
+        cpu_port(cfg, trace, weights, plan, REF_N, tokens, get_buf, shared, lib)
+    times = [cpu_port(cfg, trace, weights, plan, REF_N, tokens, get_buf, shared, lib)[0] for _ in range(args.steps)]
     total = sum(times)
     v = tokens * args.steps / total
-    sample = f"{tokens} decode tokens x 24 layers per step (fp64 gate + top-4 + INT4 routed / bf16 shared FFN)"
+    sample = (f"first {tokens} of the {args.tokens} decode tokens x 24 layers per step, same trace / plan / n={REF_N} as "
+              "the GPU arm: fp64 gate + top-4, ARC, INT2 routed experts (their GPU width) + bf16 shared FFN, AVX2 threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": "qwen1.5-moe-shape decode bs=1, cpu oracle port", "tokens_per_step": tokens},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 accumulate, fp64 router",
+        "data": "synthetic",
+        "config": {"workload": "Qwen1.5-MoE-A2.7B shape decode bs=1, fixed expert budget (BASELINE configs[1])",
+                   "tokens_per_step": tokens, "trace_tokens": args.tokens, "transfer_budget_n": REF_N,
+                   "plan": list(plan.per_layer_capacity)},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_as_is": reference_as_is(cfg, trace, weights, plan.per_layer_capacity, tokens),
     }), flush=True)
 
 
@@ -226,13 +270,17 @@ def bench_prefill(peaks, rank: int) -> dict:
 
 
 def load_traffic():
-    p = os.path.join(ROOT, "profiles", "r01_k3_ncu.json")
+    """DRAM bytes per K3 launch from the committed ncu capture of this K3 on the bench's
+    expert mix (profiles/r02_k3_bench_ncu.json, `--set full` of one launch); ncu replays
+    a launch, so this is a per-launch count taken outside the timed run.  None if absent."""
+    p = os.path.join(ROOT, "profiles", "r02_k3_bench_ncu.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            d = json.load(open(p))
+            return d.get("dram_bytes_per_launch"), d.get("source", "profiles/r02_k3_bench_ncu.json")
         except Exception:
-            return None
-    return None
+            return None, None
+    return None, None
 
 
 def main():
@@ -242,7 +290,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--tokens", type=int, default=256)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-tokens", type=int, default=8)
+    ap.add_argument("--ref-tokens", type=int, default=16)
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -367,19 +415,32 @@ def main():
         res.y = None
     e2e = T / float(np.mean(e2e_times)) * world if e2e_times else None
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and not args.no_cpu:
+        # cpu_baseline: the CPU restatement of the same path on the host cores, on the first
+        # cpu_tokens tokens with the store's own packed experts; its schedule over the whole
+        # trace is also the trace-parity check of the engine's first timed step's decisions
         from oracle import fate_oracle as O
         lib = O.cpu_lib()
         cores = lib.fate_cpu_threads(0)
-        getb = lambda l, e: store.packed(l, e, 4).numpy()  # noqa: E731
-        shb = lambda l: store.shared_buffer(l).cpu().numpy()  # noqa: E731
-        sh_cache = {l: shb(l) for l in range(cfg.num_layers)}
-        cpu_decode(cfg, trace, weights, getb, lambda l: sh_cache[l], 2, lib)
-        secs = cpu_decode(cfg, trace, weights, getb, lambda l: sh_cache[l], args.cpu_tokens, lib)
+        sh_cache = {l: store.shared_buffer(l).cpu().numpy() for l in range(cfg.num_layers)}
+        getb = lambda l, e, b: store.packed(l, e, b).numpy()  # noqa: E731
+        cpu_port(cfg, trace, weights, plan, n, 2, getb, lambda l: sh_cache[l], lib)
+        secs, _ = cpu_port(cfg, trace, weights, plan, n, args.cpu_tokens, getb, lambda l: sh_cache[l], lib)
         cpu = {"value": args.cpu_tokens / secs, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"first {args.cpu_tokens} tokens of the same trace, 24 layers (fp64 gate + top-4 + "
-                         "dequant-fused INT4 routed + bf16 shared FFN, C threads over rows)"}
+               "sample": f"first {args.cpu_tokens} tokens of the same trace x 24 layers: fp64 gate + top-4, ARC, "
+                         "the routed experts in the width the GPU computed them in + bf16 shared FFN "
+                         "(AVX2 C threads over rows)"}
+        _, port_logs = cpu_port(cfg, trace, weights, plan, n, T, None, None, lib, ffn=False)
+        eng.reset_cache()
+        vlogs = eng.decode(gd, chd, want_logs=True).logs
+        keys = ("chosen", "hits", "ondemand", "victims")
+        bad = sum(1 for a_, b_ in zip(vlogs, port_logs)
+                  if tuple(a_[k_] for k_ in keys) != tuple(b_[k_] for k_ in keys) or a_["fmt_bits"] != b_["fmt_bits"]
+                  or (n > 0 and a_.get("pred") != b_.get("pred")))
+        parity = {"trace_parity": bad == 0 and len(vlogs) == len(port_logs), "steps": len(vlogs),
+                  "mismatched_steps": bad, "fields": list(keys) + ["fmt_bits"] + (["pred"] if n > 0 else []),
+                  "against": "oracle.port_decode schedule over the whole timed trace (cold cache)"}
     # expert-sharded peer-fetch mode (BASELINE configs[4]): each rank
     # homes (l*E+e) mod G of the experts in its HBM; misses are device/peer copies
     peer = None
@@ -429,14 +490,19 @@ def main():
                        "l2": "inputs larger than L2 (1.95 GB slot pool + 12.5 GB pinned host pools)",
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic(),
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic()[0],
+                         "traffic_source": load_traffic()[1],
                          "kernel": "K3 ffn_up+ffn_down (dequant-fused SwiGLU GEMV)",
                          "bytes_per_launch": k3_bytes, "ms_per_launch": k3_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
             "cpu_baseline": cpu,
+            "trace_parity": parity["trace_parity"] if parity else None,
+            "trace_parity_detail": parity,
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b}
             if e2e else None,
-            "gpu_launches": int(args.steps * (3 * agg["steps"] + 2)),
+            # per decode step K1 + the deferred ARC update + K3; per run run_begin + the final ARC flush
+            # (agg["steps"] already sums the steps of all timed runs)
+            "gpu_launches": int(3 * agg["steps"] + 2 * args.steps),
             "clocks": clocks,
             "hit_rate_cache": agg["cache_hits"] / agg["accesses"],
             "hit_rate_combined": (agg["cache_hits"] + agg["arrival_hits"]) / agg["accesses"],

@@ -562,15 +562,56 @@ def unpack_buffer(buf: np.ndarray, H: int, I: int, bits: int) -> dict:
         c0 = lay["c" + j]
         if bits == 16:
             raw = p[c0:c0 + 2 * n].view(np.uint16).astype(np.uint32) << 16
-            out["w" + j] = raw.view(np.float32).astype(np.float64).reshape(shapes[j])
+            w = raw.view(np.float32).astype(np.float64)
+            out["w" + j] = w.reshape(shapes[j]) if j != "2" else w2_from_slabs(w, H, I, W2_SLAB_BF16)
             continue
         codes = p[c0:c0 + n * bits // 8]
         sz = p[lay["s" + j]:lay["s" + j] + n // 64 * 8].view(np.float32).reshape(-1, 2)
-        out["codes" + j] = codes
-        out["sz" + j] = sz
-        out["w" + j] = dequantize(codes, sz[:, 0].astype(np.float64), sz[:, 1].astype(np.float64), bits,
-                                  shapes[j])
+        if j == "2":
+            # slab-major W2: group order (slab, row) -> the reference's row-major (row, slab)
+            g = (n * bits // 8) // (n // 64)
+            codes = codes.reshape(I // 64, H, g).transpose(1, 0, 2).reshape(-1)
+            sz = sz.reshape(I // 64, H, 2).transpose(1, 0, 2).reshape(-1, 2)
+        out["codes" + j] = np.ascontiguousarray(codes)
+        out["sz" + j] = np.ascontiguousarray(sz)
+        out["w" + j] = dequantize(out["codes" + j], out["sz" + j][:, 0].astype(np.float64),
+                                  out["sz" + j][:, 1].astype(np.float64), bits, shapes[j])
     return out
+
+
+W2_SLAB_BF16 = 8  # bf16 W2 slab width of the packed format (quantized: 64 = one group)
+
+
+def pack_buffer(w1: np.ndarray, w3: np.ndarray, w2: np.ndarray, bits: int, layer: int = 0,
+                expert: int = 0) -> np.ndarray:
+    """The packed expert buffer in numpy (test / CPU-baseline use): 256-byte header,
+    W1 / W3 row-major, W2 slab-major, quantized with the reference's quantize."""
+    I, H = w1.shape
+    lay = buffer_layout(H, I, bits)
+    buf = np.zeros(256 + lay["payload"], np.uint8)
+    buf[:24].view(np.int32)[:] = [np.int32(np.uint32(0xFA7EB200).view(np.int32)), bits, layer, expert, H, I]
+    p = buf[256:]
+    C = W2_SLAB_BF16 if bits == 16 else 64
+    w2s = np.asarray(w2, np.float32).reshape(H, I // C, C).transpose(1, 0, 2).reshape(-1)
+    for j, w in (("1", w1), ("3", w3), ("2", w2s)):
+        w = np.asarray(w, np.float32).reshape(-1)
+        c0 = lay["c" + j]
+        if bits == 16:
+            u = w.view(np.uint32)
+            # round-to-nearest-even fp32 -> bf16 (as __float2bfloat16_rn)
+            r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+            p[c0:c0 + 2 * w.size] = r.view(np.uint8)
+            continue
+        codes, sc, zr = quantize(w.astype(np.float64), bits)
+        p[c0:c0 + codes.size] = codes
+        sz = np.stack([sc.astype(np.float32), zr.astype(np.float32)], axis=1).reshape(-1)
+        p[lay["s" + j]:lay["s" + j] + 4 * sz.size] = sz.view(np.uint8)
+    return buf
+
+
+def w2_from_slabs(flat: np.ndarray, H: int, I: int, C: int) -> np.ndarray:
+    """Slab-major W2 (slab s = columns [s*C, s*C+C) of all H rows) back to [H, I]."""
+    return np.ascontiguousarray(flat.reshape(I // C, H, C).transpose(1, 0, 2).reshape(H, I))
 
 
 # ---------------------------------------------------------------------------
@@ -596,11 +637,20 @@ def cpu_lib():
     return lib
 
 
+def cpu_scratch_floats(H: int, I: list) -> int:
+    """Scratch of fate_cpu_ffn: activations + their group sums + x's group sums."""
+    tot = int(sum(I))
+    return tot + tot // 64 + H // 64
+
+
 def cpu_ffn(lib, x: np.ndarray, bufs: list, I: list, bits: list, w: list, scratch: np.ndarray) -> np.ndarray:
     import ctypes
 
     n = len(bufs)
     H = x.shape[0]
+    need = cpu_scratch_floats(H, I)
+    if scratch.dtype != np.float32 or scratch.size < need:
+        raise ValueError(f"cpu_ffn scratch needs {need} float32, got {scratch.size} {scratch.dtype}")
     y = np.empty(H, np.float32)
     arr = (ctypes.c_void_p * n)(*[b.ctypes.data for b in bufs])
     f = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))  # noqa: E731
@@ -608,3 +658,74 @@ def cpu_ffn(lib, x: np.ndarray, bufs: list, I: list, bits: list, w: list, scratc
     lib.fate_cpu_ffn(f(xc), H, n, arr, (ctypes.c_int * n)(*I), (ctypes.c_int * n)(*bits), (ctypes.c_float * n)(*w),
                      f(y), f(scratch))
     return y
+
+
+# ---------------------------------------------------------------------------
+# CPU restatement of the whole executed decode path (bench cpu_baseline /
+# --impl reference legs): schedule + FFN, timed together
+
+
+def port_decode(gate_in, mats, taus, caps, k: int, n: int, knobs: StrategyKnobs, get_buf, shared_buf, H: int,
+                I: int, Is: int, lib, tokens: int, ffn: bool = True) -> list:
+    """Per (token, layer) step: the fp64 gate and top-k (gatesim.py:113-123,
+    core.py:159-163), the cross-layer prediction entries[:n] issued for layer+1
+    minus residents (pipeline.py:390-404, predict.py:92-107), the hit /
+    prefetched / on-demand split (pipeline.py:441-459), the expert FFN of the
+    chosen experts in the width their copy has (a cache slot keeps the width
+    that landed; prefetch = decode_bits, miss = ondemand_bits) plus the shared
+    expert with weight 1 (C threads, oracle/ffn_cpu.c), then update_after_layer
+    (cache.py:212-215).  Returns the per-step decision log.
+
+    get_buf(layer, expert, bits) -> packed buffer; shared_buf(layer) -> packed
+    bf16 shared expert (or None when Is == 0)."""
+    L = len(caps)
+    arcs = [Arc(c) for c in caps]
+    fmt = [dict() for _ in range(L)]
+    issued: dict = {}
+    logs = []
+    sizes = [I] * k + ([Is] if Is else [])
+    scratch = np.empty(cpu_scratch_floats(H, sizes), np.float32)
+    sH = np.sqrt(H)
+    for t in range(tokens):
+        for l in range(L):
+            h = gate_in[t, l]
+            w = gate_routing(mats[l], taus[l], h)
+            ch = sorted(top_k(w, k))
+            rec = {"chosen": ch}
+            if n > 0 and knobs.kind == "fate" and l + 1 < L:
+                wn = gate_routing(mats[l + 1], taus[l + 1], h)
+                lst = predicted_list(wn, knobs.policy_kind, knobs.q, k)[:n]
+                res_n = arcs[l + 1].resident()
+                issued[(t, l + 1)] = {e for e in lst if e not in res_n}
+                rec["pred"] = lst
+            res = arcs[l].resident()
+            iss = issued.pop((t, l), set())
+            bits, hits, od = [], [], []
+            for e in ch:
+                if e in res:
+                    bits.append(fmt[l][e])
+                    hits.append(e)
+                elif e in iss:
+                    bits.append(knobs.prefetch_bits)
+                else:
+                    bits.append(knobs.ondemand_bits)
+                    od.append(e)
+            if ffn:
+                x = (sH * h).astype(np.float32)
+                bufs = [get_buf(l, e, b) for e, b in zip(ch, bits)]
+                wts = [float(w[e]) for e in ch]
+                if Is:
+                    bufs.append(shared_buf(l))
+                    wts.append(1.0)
+                cpu_ffn(lib, x, bufs, sizes, bits + ([16] if Is else []), wts, scratch)
+            victims = []
+            for e, b in zip(ch, bits):
+                hit, v = arcs[l].access(e)
+                if v is not None:
+                    victims.append(v)
+                    fmt[l].pop(v, None)
+                if not hit and arcs[l].c >= 1:
+                    fmt[l][e] = b
+            rec.update({"hits": hits, "ondemand": od, "victims": victims, "fmt_bits": bits})
+            logs.append(rec)
+    return logs

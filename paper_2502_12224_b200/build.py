@@ -17,6 +17,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# FATE_PROF=1 compiles the kernels' phase timestamps in (profiling builds only;
+# the shipped library carries no instrumentation)
+if os.environ.get("FATE_PROF"):
+    FLAGS = FLAGS + ["-DFATE_PROF"]
 
 
 def sources() -> list[str]:

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <deque>
 #include <mutex>
 #include <string>
@@ -67,6 +68,30 @@ static int resolve_driver() {
   p_wait32 = (PFN_wait32)a;
   p_write32 = (PFN_write32)b;
   return FATE_OK;
+}
+
+// Launch-serialised execution (a profiler such as ncu / compute-sanitizer
+// injected through CUDA_INJECTION64_PATH, CUDA_LAUNCH_BLOCKING=1, or
+// FATE_PROFILE_SERIAL): a kernel launch may block the calling thread until the
+// kernel has run, so the engine never enqueues a kernel behind a stream wait
+// that this same thread must release.  Each step's expert compute is launched
+// only after the host has seen its transfers land.  Same decisions and
+// results; only the copy/compute overlap is lost.
+static bool serial_launches() {
+  static const bool v = [] {
+    const char *b = getenv("CUDA_LAUNCH_BLOCKING");
+    const char *inj = getenv("CUDA_INJECTION64_PATH");
+    const char *pre = getenv("LD_PRELOAD");
+    bool prof = (inj && *inj) || (pre && (strstr(pre, "TreeLauncher") || strstr(pre, "nsight") ||
+                                          strstr(pre, "Injection") || strstr(pre, "sanitizer")));
+    for (char **e = environ; !prof && e && *e; ++e)
+      prof = strncmp(*e, "NV_COMPUTE_PROFILER", 19) == 0 || strncmp(*e, "NSIGHT_COMPUTE", 14) == 0 ||
+             strncmp(*e, "NV_TPS", 6) == 0;
+    const bool on = getenv("FATE_PROFILE_SERIAL") != nullptr || (b && atoi(b) != 0) || prof;
+    if (on && getenv("FATE_DEBUG")) fprintf(stderr, "[fate] launch-serialised mode\n");
+    return on;
+  }();
+  return v;
 }
 
 static int cu_status(CUresult r, const char *what) {
@@ -151,6 +176,11 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
 // [0] block 0 start, [1] tail start, [2] state staged, [3] routed, [4] split,
 // [5] predicted, [6] message posted
 __device__ unsigned long long g_k1_prof[16];
+#ifdef FATE_PROF
+#define K1_STAMP(i) (g_k1_prof[i] = gtime1())
+#else
+#define K1_STAMP(i) ((void)0)  // phase stamps are compiled in only with -DFATE_PROF
+#endif
 
 __device__ __forceinline__ unsigned long long gtime1() {
   unsigned long long t;
@@ -195,8 +225,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_prof[0] = gtime1();
-  if (threadIdx.x == 0 && blockIdx.x == 1) g_k1_prof[10] = gtime1();
+  if (blockIdx.x == 0 && threadIdx.x == 0) K1_STAMP(0);
+  if (threadIdx.x == 0 && blockIdx.x == 1) K1_STAMP(10);
   if (blockIdx.x > 0) {
     // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
     const int lrow = row < E ? layer : layer + 1;
@@ -239,7 +269,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (threadIdx.x == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(&d.ctrl->arrive, 1u);
-      if (prev == (unsigned)n_rows - 1u) g_k1_prof[11] = gtime1();  // last arrival
+      if (prev == (unsigned)n_rows - 1u) K1_STAMP(11);  // last arrival
     }
     return;
   }
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     while (*(volatile uint32_t *)&C.arrive < (uint32_t)n_rows) {
     }
     __threadfence();
-    g_k1_prof[1] = gtime1();
+    K1_STAMP(1);
     S.c_free_top = *(volatile int32_t *)&C.free_top;
   }
   __syncthreads();
@@ -305,27 +335,35 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   const int k = d.k;
   const int step = S.c_step;
   fate_step_log *lg = log ? log + step : nullptr;
-  if (lane == 0) g_k1_prof[2] = gtime1();
+  if (lane == 0) K1_STAMP(2);
   // (2) routing of layer l (gatesim.py:113-123, core.py:159-163): S.w / S.ord above
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   // chosen ids in ascending order (pipeline.py:441 iterates sorted(chosen)):
-  // lane i < k owns ord[i]; its position = #{j < k : ord[j] < ord[i]}
+  // lane i < k owns ord[i]; its position = #{j < k : ord[j] < ord[i]}.  When
+  // the trace supplies the chosen set (record.chosen, pipeline.py:422) it is
+  // what the split and the ARC update use, as in the reference; the recomputed
+  // top-k only feeds the mismatch counter (routing weights and predictions
+  // always come from the device's fp64 router).
   {
     const int mine = lane < k ? S.ord[lane] : 0x7fffffff;
     int pos = 0;
     for (int j = 0; j < k; ++j) pos += __shfl_sync(FULL, mine, j) < mine;
-    if (lane < k) {
-      S.chosen[pos] = mine;
-      S.is_chosen[mine] = 1;
-    }
+    if (lane < k) S.csrc[pos] = mine;  // the recomputed set, ascending
+  }
+  __syncwarp();
+  const int own = lane < k ? S.csrc[lane] : 0;
+  if (lane < k) {
+    const int use = trace_chosen ? tchosen[lane] : own;
+    S.chosen[lane] = use;
+    S.is_chosen[use] = 1;
   }
   __syncwarp();
   const bool act = lane < k;
   const int ce = act ? S.chosen[lane] : 0;
   {
     int mism = 0;
-    if (trace_chosen && act) mism = tchosen[lane] != ce;
+    if (trace_chosen && act) mism = own != ce;
     mism = __any_sync(FULL, mism);
     // recall of the prediction made one step earlier (pipeline.py:433-436)
     const bool chk = S.c_pred_valid && S.c_pred_layer == layer;
@@ -344,7 +382,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
       }
     }
   }
-  if (lane == 0) g_k1_prof[3] = gtime1();
+  if (lane == 0) K1_STAMP(3);
   // (3) hit / prefetched / on-demand split (pipeline.py:441-459), one lane per chosen expert
   StepMsg *msg = d.ring + (step % kRing);
   int top = S.c_free_top;
@@ -411,7 +449,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     top += __popc(m);
     n_drop += __popc(m);
   }
-  if (lane == 0) g_k1_prof[4] = gtime1();
+  if (lane == 0) K1_STAMP(4);
   // (5) cross-layer prediction for layer l+1 (predict.py:92-107, pipeline.py:390-404)
   int n_pf = 0, n_pred = -1;
   if (d.use_predictor && d.policy == 2) {
@@ -494,7 +532,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     atomicAdd(&d.stats->ondemand_issued, (unsigned long long)n_od);
     atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
   }
-  if (lane == 0) g_k1_prof[5] = gtime1();
+  if (lane == 0) K1_STAMP(5);
   // (6) the K3 batch: routed experts weighted by their full-softmax routing
   // weight (not renormalised), plus the shared expert with weight 1.
   // storage width of every buffer is known here (hit: the slot's tagged width;
@@ -506,7 +544,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (lane == 0) {
     int n = k, off = k * d.I;
     if (S.shared_present) {
-      B.e[n] = FfnExpert{d.shared_k3[layer], 1.0f, d.I_shared, d.shared_bits, off, d.shared_layout};
+      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, d.shared_bits, off, 0};
       off += d.I_shared;
       ++n;
     }
@@ -541,8 +579,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     C.cur_layer = layer;
     C.step = step + 1;
     if (layer == L - 1) C.next_token = token + 1;
-    g_k1_prof[6] = gtime1();
-    g_k1_prof[7] = gtime1();
+    K1_STAMP(6);
+    K1_STAMP(7);
   }
 }
 
@@ -552,9 +590,9 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
 __global__ void arc_update_kernel(EngineDev d, fate_step_log *log) {
   __shared__ ArcLayer arc_sm;
   __shared__ int32_t rel[4 * KMAX + 4];
-  if (threadIdx.x == 0) g_k1_prof[8] = gtime1();
+  if (threadIdx.x == 0) K1_STAMP(8);
   if (d.ctrl->prev_valid) apply_prev_update(d, &arc_sm, log, rel);
-  if (threadIdx.x == 0) g_k1_prof[9] = gtime1();
+  if (threadIdx.x == 0) K1_STAMP(9);
 }
 
 // Standalone ARC accesses (update_after_layer / arc_access API).  Newly
@@ -700,7 +738,7 @@ struct fate_engine {
   uint8_t *pool = nullptr;
   int32_t *caps_dev = nullptr;
   int32_t *scratch_i = nullptr;  // small scratch for standalone calls
-  float *a_scratch = nullptr;
+  void *k3_scratch = nullptr;  // K3 per-CTA partials + grid-barrier word (this engine's launches only)
   // mapped pinned host memory
   StepMsg *ring_host = nullptr;
   volatile uint32_t *ready_host = nullptr;     // [L]
@@ -714,8 +752,6 @@ struct fate_engine {
   int64_t host_stride[17] = {};
   std::vector<const uint8_t *> shared_dev;
   const uint8_t **shared_table_dev = nullptr;
-  std::vector<uint8_t *> shared_k3;            // owned K3 copies (bf16: W2 slab-major)
-  const uint8_t **shared_k3_table_dev = nullptr;
   int32_t *pf_shared_I = nullptr;
   cudaStream_t cstream = nullptr, xstream = nullptr, xstream2 = nullptr;  // compute, two copy streams
   cudaEvent_t xlast[2] = {nullptr, nullptr};  // last copy submitted on each copy stream
@@ -858,8 +894,7 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
                o_bb = carve((size_t)nbuf * 4),
                o_ctrl = carve(sizeof(Ctrl)), o_st = carve(sizeof(DevStats)), o_lg = carve(2 * EMAX * 8),
                o_x = carve(ffn_xlay_floats(H) * 4), o_b = carve(sizeof(FfnBatch)), o_caps = carve((size_t)L * 4),
-               o_sh = carve((size_t)L * 8), o_sh3 = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
-               o_a = carve(ffn_alay_floats(g->max_total_I) * 4),
+               o_sh = carve((size_t)L * 8), o_si = carve((2 * FATE_MAX_EXPERTS + 2) * 4 * 2),
                o_ec = carve((size_t)std::max(L - 1, 1) * E * E * 4), o_et = carve((size_t)std::max(L - 1, 1) * E * 4);
   FATE_CUDA(cudaMalloc(&g->dev_block, off));
   FATE_CUDA(cudaMemset(g->dev_block, 0, off));
@@ -882,19 +917,19 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   g->caps_dev = (int32_t *)(base + o_caps);
   g->shared_table_dev = (const uint8_t **)(base + o_sh);
   d.shared = cfg->shared_intermediate ? g->shared_table_dev : nullptr;
-  g->shared_k3_table_dev = (const uint8_t **)(base + o_sh3);
-  d.shared_k3 = g->shared_k3_table_dev;
-  d.shared_layout = cfg->shared_bits == 16 ? 1 : 0;
   g->scratch_i = (int32_t *)(base + o_si);
-  g->a_scratch = (float *)(base + o_a);
   d.eap_counts = (int32_t *)(base + o_ec);
   d.eap_totals = (int32_t *)(base + o_et);
   g->eap_bytes = (size_t)((o_et - o_ec) + (size_t)std::max(L - 1, 1) * E * 4);
   FATE_CUDA(cudaMalloc(&g->pool, (size_t)nbuf * g->buf_stride));
   d.pool = g->pool;
+  {
+    const size_t kb = ffn_scratch_bytes(H);
+    FATE_CUDA(cudaMalloc(&g->k3_scratch, kb));
+    FATE_CUDA(cudaMemset(g->k3_scratch, 0, kb));
+  }
   FATE_CUDA(cudaMemcpy(g->caps_dev, g->caps.data(), L * 4, cudaMemcpyHostToDevice));
   g->shared_dev.assign(L, nullptr);
-  g->shared_k3.assign(L, nullptr);
   // mapped pinned host memory: mailbox ring, ready flags, copy counter
   void *p = nullptr;
   FATE_CUDA(cudaHostAlloc(&p, sizeof(StepMsg) * kRing, cudaHostAllocMapped));
@@ -965,8 +1000,7 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   if (g->ev_arc) cudaEventDestroy(g->ev_arc);
   cudaFree(g->pool);
   cudaFree(g->dev_block);
-  for (auto *p : g->shared_k3)
-    if (p) cudaFree(p);
+  if (g->k3_scratch) cudaFree(g->k3_scratch);
   if (g->pf_block) cudaFree(g->pf_block);
   cudaFreeHost(g->ring_host);
   cudaFreeHost((void *)g->ready_host);
@@ -1005,17 +1039,6 @@ extern "C" int fate_engine_set_host_pool(fate_engine *g, int bits, const uint8_t
   g->host_pool[bits] = base;
   g->host_stride[bits] = stride;
   return FATE_OK;
-}
-
-// W2 [H, I] row-major -> column slabs: slab t = columns [t*kSlabCols, t*kSlabCols + w_t)
-// of all H rows, row-major inside (w_t = kSlabCols, the last one narrower).
-__global__ void slab_w2_kernel(const __nv_bfloat16 *__restrict__ w2, int H, int I, __nv_bfloat16 *__restrict__ out) {
-  const int64_t n = (int64_t)H * I;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int h = (int)(i / I), c = (int)(i % I);
-    const int k0 = c / kSlabCols * kSlabCols, w = min(kSlabCols, I - k0);
-    out[(int64_t)H * k0 + (int64_t)h * w + (c - k0)] = w2[i];
-  }
 }
 
 extern "C" int fate_engine_set_expert_sources(fate_engine *g, int bits, const uint8_t *const *srcs) {
@@ -1080,22 +1103,6 @@ extern "C" int fate_engine_set_shared(fate_engine *g, int layer, const uint8_t *
   g->shared_dev[layer] = buf_dev;
   FATE_CUDA(cudaMemcpy(g->shared_table_dev, g->shared_dev.data(), g->cfg.num_layers * sizeof(void *),
                        cudaMemcpyHostToDevice));
-  // K3's own copy: bf16 W2 re-laid into column slabs (one bulk copy per phase-B tile)
-  const int H = g->cfg.hidden_dim, Is = g->cfg.shared_intermediate, bits = g->cfg.shared_bits;
-  const int64_t bytes = buffer_bytes(H, Is, bits);
-  if (!g->shared_k3[layer]) FATE_CUDA(cudaMalloc(&g->shared_k3[layer], bytes));
-  uint8_t *dst = g->shared_k3[layer];
-  FATE_CUDA(cudaMemcpy(dst, buf_dev, bytes, cudaMemcpyDeviceToDevice));
-  if (bits == 16) {
-    const Layout Lo = make_layout(H, Is, 16);
-    const __nv_bfloat16 *w2 = reinterpret_cast<const __nv_bfloat16 *>(buf_dev + FATE_HEADER_BYTES + Lo.c2);
-    __nv_bfloat16 *o2 = reinterpret_cast<__nv_bfloat16 *>(dst + FATE_HEADER_BYTES + Lo.c2);
-    slab_w2_kernel<<<148 * 4, 256, 0, g->cstream>>>(w2, H, Is, o2);
-    FATE_CHECK_LAUNCH("slab_w2_kernel");
-    FATE_CUDA(cudaStreamSynchronize(g->cstream));
-  }
-  std::vector<const uint8_t *> t(g->shared_k3.begin(), g->shared_k3.end());
-  FATE_CUDA(cudaMemcpy(g->shared_k3_table_dev, t.data(), g->cfg.num_layers * sizeof(void *), cudaMemcpyHostToDevice));
   return FATE_OK;
 }
 
@@ -1190,6 +1197,22 @@ struct Channel {
 
   int bytes_of(int bits) const { return (int)buffer_bytes(g->cfg.hidden_dim, g->cfg.intermediate_dim, bits); }
 
+  // launch-serialised mode: completions are seen through events and every flag
+  // is set by this thread (no stream memory operations at all)
+  bool serial = false;
+  std::vector<cudaEvent_t> sev;  // one per in-flight slot
+  std::vector<int> sev_free;
+  ~Channel() {
+    for (auto &e : sev) cudaEventDestroy(e);
+  }
+  int init_serial() {
+    serial = true;
+    sev.resize(g->cfg.max_inflight + 4);
+    for (auto &e : sev) FATE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int i = (int)sev.size() - 1; i >= 0; --i) sev_free.push_back(i);
+    return FATE_OK;
+  }
+
   uint32_t submitted_s[2] = {0u, 0u};
   int next_stream = 0;
 
@@ -1223,9 +1246,18 @@ struct Channel {
       if (evi >= 0) FATE_CUDA(cudaEventRecord(ev[evi + 1], s));
       // landed marks are read only for queued prefetches (K1's arrival check):
       // on-demand copies skip the extra stream op between back-to-back copies
-      if (t.kind == 0) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
+      if (t.kind == 0 && !serial) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
       FATE_CUDA(cudaEventRecord(g->xlast[si], s));
       (dsrc ? d2d_bytes : h2d_bytes) += bytes;
+    }
+    if (serial) {
+      // completion through an event; the host sets the step's flag when it reaps
+      const int se = sev_free.back();
+      sev_free.pop_back();
+      FATE_CUDA(cudaEventRecord(sev[se], s));
+      ++submitted;
+      inflight.push_back(Inflight{submitted, t, evi, si, (uint32_t)se});
+      return FATE_OK;
     }
     // the step's wait flag is released by the copy streams themselves right
     // after the last transfer the step needs (the host also sets it when reaping)
@@ -1240,10 +1272,17 @@ struct Channel {
     return FATE_OK;
   }
 
+  bool front_done() {
+    const Inflight &f = inflight.front();
+    if (serial) return cudaEventQuery(sev[f.sseq]) == cudaSuccess;
+    const uint32_t c = f.stream ? *g->copy_done_host2 : *g->copy_done_host;
+    return (int32_t)(c - f.sseq) >= 0;
+  }
+
   void reap() {
-    const uint32_t c[2] = {*g->copy_done_host, *g->copy_done_host2};
-    while (!inflight.empty() && (int32_t)(c[inflight.front().stream] - inflight.front().sseq) >= 0) {
+    while (!inflight.empty() && front_done()) {
       Inflight &f = inflight.front();
+      if (serial) sev_free.push_back((int)f.sseq);
       if (f.ev >= 0) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, ev[f.ev], ev[f.ev + 1]) == cudaSuccess) copy_ms += ms;
@@ -1310,6 +1349,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   Channel ch;
   ch.g = g;
   ch.timed = timed;
+  if (serial_launches())
+    if (int st = ch.init_serial()) return st;
   std::vector<cudaEvent_t> kev;  // per step: K1 start, K1 end, K3 start (after the wait), K3 end
   if (timed) {
     ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
@@ -1334,13 +1375,13 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] run_begin done\n");
   int launched = 0, processed = 0, k3_next = 0;
   const int lookahead = 4;
-  const bool serial = getenv("FATE_PROFILE_SERIAL") != nullptr;
+  const bool serial = serial_launches();
   // K3 of step s (routed + shared experts), after the step's wait
   auto ffn_step = [&](int s) -> int {
     const int t = s / L, l = s % L;
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
-    FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->a_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                       g->max_total_I, &g->d.stats->ffn_bytes, cs));
+    FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->k3_scratch, y_dev + ((int64_t)t * L + l) * H, H,
+                                       &g->d.stats->ffn_bytes, cs));
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
     return FATE_OK;
   };
@@ -1397,8 +1438,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       FATE_CHECK_LAUNCH("arc_update_kernel (step update)");
       FATE_CUDA(cudaEventRecord(g->ev_arc, g->astream));
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
-      FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u,
-                                  CU_STREAM_WAIT_VALUE_GEQ));
+      // serial mode: no stream wait at all (the host enqueues K3 only once the flag is set)
+      if (!serial)
+        FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u, CU_STREAM_WAIT_VALUE_GEQ));
       if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
       if (!serial && (status = ffn_step(s))) break;
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K3 step %d\n", s);
@@ -1743,11 +1785,19 @@ __global__ void __launch_bounds__(1024) prefill_plan_kernel(EngineDev d, PfScrat
         c[j] = c[j - 1];
         c[j - 1] = x;
       }
+    // the trace's chosen set (record.chosen, ascending) drives actives and the
+    // ARC update when supplied, as in the reference (pipeline.py:620-631); the
+    // recomputed top-k only feeds the mismatch counter
+    if (trace_chosen)
+      for (int j = 0; j < k; ++j) {
+        const int tc = trace_chosen[((int64_t)t * L + layer) * k + j];
+        if (tc != c[j]) atomicExch(&mism, 1);
+        c[j] = tc;
+      }
     for (int j = 0; j < k; ++j) {
       s.chosen[t * k + j] = c[j];
       s.cw[t * k + j] = (float)s.routing[(int64_t)t * E + c[j]];
       atomicAdd(&cnt[c[j]], 1);
-      if (trace_chosen && trace_chosen[((int64_t)t * L + layer) * k + j] != c[j]) atomicExch(&mism, 1);
     }
     if (predict)
       for (int j = 0; j < k; ++j) atomicAdd(&pcnt[s.order_n[(int64_t)t * E + j]], 1);
@@ -2080,6 +2130,8 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   Channel ch;
   ch.g = g;
   ch.timed = timed;
+  if (serial_launches())
+    if (int st = ch.init_serial()) return st;
   std::vector<cudaEvent_t> kev;
   if (timed) {
     ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
@@ -2244,7 +2296,21 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
     for (int e = 0; e < E; ++e) pf_bits_cur[e] = 0;
     for (int i = 0; i < m.n_pf; ++i) pf_bits_cur[m.pf_e[i]] = m.pf_bits_each[i];
     // expert compute for layer l once every needed copy landed
-    FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), 1u, CU_STREAM_WAIT_VALUE_GEQ));
+    if (serial_launches()) {
+      // launch-serialised mode: the host waits for the flag, then enqueues K4
+      while (((volatile uint32_t *)g->ready_host)[l] < 1u) {
+        if ((status = ch.pump())) break;
+        _mm_pause();
+        if (std::chrono::steady_clock::now() - last_progress > std::chrono::seconds(60)) {
+          status = FATE_ETIMEOUT;
+          set_error("fate_engine_prefill: transfers of a layer never completed (serial mode)");
+          break;
+        }
+      }
+      if (status) break;
+    } else {
+      FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), 1u, CU_STREAM_WAIT_VALUE_GEQ));
+    }
     if (timed) FATE_CUDA(cudaEventRecord(kev[4 * l + 2], cs));
     int tiles_up = 0, tiles_down = 0;
     for (int i = 0; i < m.n_active; ++i) {

@@ -71,8 +71,6 @@ struct EngineDev {
   int64_t buf_stride;
   uint8_t *pool;              // nbuf * buf_stride
   const uint8_t **shared;     // [L] shared-expert buffers (or null)
-  const uint8_t **shared_k3;  // [L] K3's copies of them (bf16: W2 slab-major, layout 1)
-  int shared_layout;          // FfnExpert.layout of shared_k3 buffers
   const double *W;            // [L, E, H]
   const double *tau;          // [L]
   ArcLayer *arc;              // [L]

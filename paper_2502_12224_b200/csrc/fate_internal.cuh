@@ -33,9 +33,18 @@ int cuda_status(cudaError_t e, const char *what);
 //   quantized (bits 8/4/2): codes w1 [I*H*b/8] | codes w3 | codes w2 [H*I*b/8]
 //                           | sz w1 [I*H/64 float2] | sz w3 | sz w2
 //   bf16 (bits 16):         w1 [I*H] | w3 [I*H] | w2 [H*I]
+// W1 / W3 are row-major [I, H] (groups of 64 along H).  W2 [H, I] is stored
+// SLAB-MAJOR: slab s holds columns [s*C, s*C + C) of all H rows, row-major
+// inside, with C = kW2SlabQuant = 64 (exactly one quantization group of the
+// reference's row-major grouping, so codes / scale / zero per group are
+// byte-identical, only the group order differs) and C = kW2SlabBf16 = 8 for
+// bf16.  K3 thereby reads the W2 columns matching a block of W1/W3 rows as one
+// contiguous bulk copy, and K4 reads a 64-column K-step of 128 rows likewise.
 // The payload size equals expert_bytes[bits] of quant.py:239-246.  A copy of
 // the whole buffer carries its own format, so a cache slot filled by an INT2
 // on-demand load is computed as INT2 (the "tag slot bits" decision).
+constexpr int kW2SlabQuant = 64;
+constexpr int kW2SlabBf16 = 8;
 constexpr uint32_t kMagic = 0xFA7EB200u;
 constexpr int kGroup = 64;
 
@@ -96,15 +105,9 @@ struct FfnExpert {
   float weight;
   int I;
   int bits;
-  int a_off;           // offset of this expert's activation vector in scratch
-  int layout;          // 0: row-major; 1: bf16 W2 stored in column slabs of kSlabCols (K3-only copy)
+  int a_off;           // offset of this expert's rows in the step's concatenated intermediate dim
+  int pad;
 };
-
-// Column-slab width of the K3-only copy of a resident bf16 expert's W2
-// (= K3's phase-B K-range for bf16: 96 chunks x 8 columns): slab t holds
-// columns [t*kSlabCols, ...) of all H rows contiguously, so any phase-B tile
-// (consecutive rows of one K-range) is a single bulk copy.
-constexpr int kSlabCols = 768;
 
 constexpr int kMaxFfnExperts = FATE_MAX_TOPK + 2;
 
@@ -112,21 +115,23 @@ struct FfnBatch {
   int n;
   int H;
   int total_I;
-  unsigned int work;   // K3 phase-A tile counter (dynamic scheduling); zero before each launch
+  unsigned int work;   // unused (kept zero)
   FfnExpert e[kMaxFfnExperts];
 };
 static_assert(sizeof(FfnBatch) % 16 == 0, "K3 copies the batch with 16-byte loads");
 
-// K3 launch (one kernel per step).  xlay: x in every chunk-transposed width
-// layout (ffn_xlay_floats(H) floats, see write_xlay); alay: activation layout
-// scratch (ffn_alay_floats(max_total_I) floats).  The batch is in DEVICE memory.
-cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
-                              int max_total_I, cudaStream_t s);
-cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev,
-                                     int H, int max_total_I, unsigned long long *bytes_stat, cudaStream_t s);
+// K3 launch (one cooperative kernel per step).  xlay: x in every
+// chunk-transposed width layout (ffn_xlay_floats(H) floats, see write_xlay);
+// scratch: ffn_scratch_bytes(H) bytes owned by ONE caller (per-CTA partial y
+// rows + the grid-barrier word; zero-initialised once, launches serialised on
+// one stream).  The batch is in DEVICE memory.
+cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
+                              cudaStream_t s);
+cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev,
+                                     int H, unsigned long long *bytes_stat, cudaStream_t s);
 cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s);
 size_t ffn_xlay_floats(int H);
-size_t ffn_alay_floats(int max_total_I);
+size_t ffn_scratch_bytes(int H);
 
 // x (in shared memory) -> the four chunk-transposed layouts + chunk sums, by
 // a whole thread block: slot s (chunk width 8 << s) at xlay + s*(H/4 + H/32) float4.

@@ -4,26 +4,32 @@
 // the step (+ the shared expert with weight 1), reading each expert's packed
 // buffer straight from HBM (cache slot or freshly landed staging slot).
 //
-// The op is a chain of GEMVs: pure HBM streaming, and the B200 design is a
-// TMA-bulk pipeline per SM:
-//  * one persistent CTA per SM: warps 0-3 produce (tile g of the stage
-//    sequence on warp g mod 4), warps 4-15 consume;
-//  * weights move global -> shared with cp.async.bulk (the TMA engine; SASS
-//    UBLKCP) into a ring of 32 KB stages completed on mbarriers, so ~100 KB
-//    per SM are in flight independently of register pressure, and every
-//    weight byte crosses HBM exactly once;
-//  * a tile is a block of contiguous rows of one projection (plus their fp32
-//    scale/zero pairs); rows of W1 and W3 with the same index share a tile so
-//    silu(u)*v is formed on chip (phase A); phase B tiles are rows of W2 of
-//    every expert, reduced over experts inside the CTA (deterministic, no atomics);
-//  * the activation vector is staged once per CTA and laid out
-//    chunk-transposed, xt[quad][chunk], so 32 lanes read 32 consecutive float4s;
-//  * dequant folds the affine map per 16-byte chunk: sum_i (z + s c_i) x_i
-//    = s * sum_i c_i x_i + z * sum_i x_i with chunk sums precomputed, i.e. one
-//    FFMA per weight element plus code extraction.
+// The op is a chain of GEMVs: pure HBM streaming.  B200 design: one
+// persistent CTA per SM (cooperative launch), a TMA-bulk ring per SM and a
+// split-K schedule with no mid-kernel dependency:
+//  * the work is cut into UNITS = (expert j, slab s of C rows of I): the C
+//    rows of W1_j and W3_j plus the matching C columns of W2_j.  The packed
+//    format stores W2 slab-major (C = 64 = one quantization group for
+//    INT8/4/2, C = 8 for bf16; fate_internal.cuh), so a unit's W2 part is
+//    one contiguous H x C block;
+//  * a CTA computes its units' activations a = w_j * silu(W1 x) * (W3 x) on
+//    chip and immediately multiplies them into its own partial y[H] (shared
+//    memory) with the W2 slab: every weight byte crosses HBM exactly once and
+//    the W2 stream never waits for other CTAs;
+//  * units are assigned statically and deterministically: quantized units
+//    round-robin, bf16 units fill every CTA to the same weighted byte count;
+//  * weights move global -> shared with cp.async.bulk (SASS UBLKCP) into a
+//    ring of 32 KB stages completed on mbarriers; warps 0-3 produce (stage g
+//    on warp g mod 4), warps 4-15 consume;
+//  * one grid barrier at the very end, then CTA c sums rows of y over the
+//    per-CTA partials in fixed CTA order: y is deterministic;
+//  * dequant folds the affine map per group: sum_i (z + s c_i) a_i =
+//    s * sum_i c_i a_i + z * sum_i a_i, codes become exact floats under the
+//    2^23 magic (PRMT / one LOP3 per code) and FFMA2 does two MACs.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "fate_internal.cuh"
@@ -32,15 +38,14 @@ namespace fate {
 namespace {
 
 constexpr int kConsumers = 12;  // consumer warps
-constexpr int kProducers = 4;   // producer warps (tile g of the stage sequence -> warp g % kProducers);
+constexpr int kProducers = 4;   // producer warps (stage g -> warp g % kProducers);
                                 // 16 warps -> 128 registers per thread (allocation in 4-warp units)
 constexpr int kThreads = 32 * (kProducers + kConsumers);
 constexpr int kStageBytes = 32 * 1024;
 constexpr int kMaxStages = 6;
-constexpr int kSubRows = 16;     // phase B rows per sub-block (r = 4m + warp%4, m < 4)
-constexpr int kMaxBChunks = 96;  // phase B 16-byte chunks per row per tile (3 groups of 32 lanes)
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kMaxUpRows = 64;
+constexpr int kRowsPerIter = 8 * kConsumers;    // quantized W2 rows per consumer sweep: 4 lanes per row
+constexpr int kRowsPerIterBf = 32 * kConsumers; // bf16 W2 rows per consumer sweep: one lane per row
 
 // ---------------------------------------------------------------------------
 // PTX helpers: mbarrier + bulk async copy (TMA, non-tensor form)
@@ -218,112 +223,128 @@ struct Ring {
   uint64_t full[kMaxStages], empty[kMaxStages];
 };
 
-// ----------------------------------------------------------------- tiles
-// Phase A tile = rows [r0, r0+nr) of W1_j and W3_j of one expert (contiguous
-// in the buffer); smem [W1 codes R*rb][W3 codes R*rb][W1 sz R*szb][W3 sz R*szb]
-// with R = rows_pt[j].  Phase B tile = columns [k0, k0+nc) of nr (<= 16)
-// consecutive rows of W2_j; smem [codes nr * nc*b/8][sz nr * nc/8] (one bulk
-// copy per row and region).  The producer publishes each stage's tile in
-// meta[stage] before arming its barrier, so consumers never search or divide.
-
-__device__ __forceinline__ int up_rows_per_tile(int64_t rb, int64_t szb) {
-  int R = (int)(kStageBytes / (2 * (rb + szb)));
-  R = R > kMaxUpRows ? kMaxUpRows : R;
-  return R >= 4 ? R / 4 * 4 : (R >= 1 ? R : 1);
-}
+// ----------------------------------------------------------------- units
+// Unit (j, s): rows [s*C, s*C + C) of W1_j / W3_j and slab s of W2_j.
+// A-piece: rows [r0, r0+nr) of the unit; smem [W1 codes nr*rb][W3 codes nr*rb]
+//          [W1 sz nr*szb][W3 sz nr*szb] (the layout up_pair reads).
+// W-piece: slab rows [h0, h0+nh); smem [codes nh*wrb][sz nh*8].
+struct ExpertPlan {
+  int C, units;         // slab width, units
+  int npa, ra;          // A-pieces per unit, rows per A-piece (last one may be shorter)
+  int npw, rw;          // W-pieces per unit, rows per W-piece
+  float cost;           // weighted bytes of one unit (balancing only)
+};
 
 struct Plan {
-  int n_a;                                  // phase A tiles (grabbed dynamically)
-  int RBB, n_blk;                           // phase B: rows per CTA row block, number of row blocks
-  int tile_off[kMaxFfnExperts + 1], rows_pt[kMaxFfnExperts];
-  int lay_off[kMaxFfnExperts + 1];          // activation layout offsets (floats)
-  int colsB[kMaxFfnExperts], ktiles[kMaxFfnExperts];  // phase B: W2 columns per tile, tiles per row set
+  ExpertPlan ep[kMaxFfnExperts];
+  int nq, ns;           // quantized units (round-robin), bf16 units (filled)
+  int q_first;          // this CTA's quantized units: q_first, q_first + G, ...
+  int nq_mine;
+  int s_lo, s_hi;       // this CTA's bf16 units [s_lo, s_hi)
 };
 
 struct TileMeta {
-  int j;      // expert; -1 = end of phase A, -2 = end of phase B
-  int r0;     // phase A: first row of W1/W3; phase B: first output row
-  int nr;     // rows in the tile
-  int k0;     // phase B: first column of W2
-  int nc;     // phase B: columns
-  int flush;  // phase B: last tile of its row sub-block
-  int pad[2];
+  int kind;   // 0: A-piece, 1: W-piece, 2: end
+  int j, s;   // expert, slab
+  int r0, nr; // A: rows within the unit; W: first slab row, rows
+  int flag;   // A: last A-piece of its unit (warps then arrive on the unit's activation barrier);
+              // W: first W-piece of its unit (warps wait on it)
+  int ub;     // activation buffer of the unit (units rotate over kActBufs)
+  int par;    // parity of that buffer's barrier for this unit
 };
 
-// Warp 0 builds the plan: lane j fills expert j, offsets by shuffle scans.
-__device__ __forceinline__ void make_plan_warp(const FfnBatch &b, Plan &p, int grid, int lane) {
-  const int H = b.H;
-  int tiles = 0, I = 0, R = 1, colsB = 1, kt = 0;
-  if (lane < b.n) {
-    const int bits = b.e[lane].bits;
-    I = b.e[lane].I;
-    R = up_rows_per_tile((int64_t)H * bits / 8, sz_row_bytes(H, bits));
-    tiles = (I + R - 1) / R;
-    // W2 columns per tile: kSubRows rows must fit one stage and a row's 16-byte
-    // chunks must fit 3 chunk groups of 32 lanes (kMaxBChunks)
-    const int per128 = 16 * bits + (bits == 16 ? 0 : 16);  // bytes per 128 columns of one row
-    int cols = kStageBytes / (kSubRows * per128) * 128;
-    const int by_chunks = kMaxBChunks * (bits == 16 ? 8 : 128 / bits);
-    cols = cols < by_chunks ? cols : by_chunks;
-    colsB = cols < I ? cols : I;
-    kt = (I + colsB - 1) / colsB;
+// W-pieces of unit k are streamed after the A-pieces of unit k+1, so a warp
+// never waits for the others' activation rows of the unit it is about to
+// multiply; four activation buffers keep every unit in flight distinct.
+constexpr int kActBufs = 4;
+
+__host__ __device__ __forceinline__ int slab_cols(int bits) { return bits == 16 ? kW2SlabBf16 : kW2SlabQuant; }
+__host__ __device__ __forceinline__ int w2_row_bytes(int bits) { return slab_cols(bits) * bits / 8; }
+__host__ __device__ __forceinline__ int w2_sz_bytes(int bits) { return bits == 16 ? 0 : 8; }
+
+// relative consumer cost per byte (quantized codes cost ALU work; bf16 streams)
+// Relative CTA time per byte.  bf16 units stream at the SM's share of HBM
+// (~44 GB/s); quantized units are bound by the consumers' dequant arithmetic
+// (measured in the K3 stage timeline: an INT2 unit of 144 KB ~10 us, an INT4
+// unit of 240 KB ~11 us), so they count ~3x / ~2.2x per byte.
+__device__ __forceinline__ float cost_per_byte(int bits) {
+  return bits == 16 ? 1.0f : bits == 8 ? 1.6f : bits == 4 ? 2.2f : 3.0f;
+}
+
+__device__ void expert_plan(const FfnExpert &e, int H, ExpertPlan &p) {
+  const int bits = e.bits, C = slab_cols(bits);
+  const int rb = H * bits / 8, szb = bits == 16 ? 0 : H / 8;
+  int rmax = kStageBytes / (2 * (rb + szb));
+  rmax = rmax < 1 ? 1 : rmax;
+  p.C = C;
+  p.units = e.I / C;
+  p.npa = (C + rmax - 1) / rmax;
+  p.ra = (C + p.npa - 1) / p.npa;
+  // W-pieces of whole 96-row blocks (w2_blocks: the whole of H when one stage holds it)
+  const int rows = kStageBytes / (w2_row_bytes(bits) + w2_sz_bytes(bits));
+  const int per = bits == 16 ? kRowsPerIterBf : kRowsPerIter;
+  p.rw = rows >= H ? H : rows / per * per;
+  p.npw = (H + p.rw - 1) / p.rw;
+  const float bytes = 2.0f * C * (rb + szb) + (float)H * (w2_row_bytes(bits) + w2_sz_bytes(bits));
+  p.cost = bytes * cost_per_byte(bits);
+}
+
+// (expert, slab) of the i-th unit of a class (quantized or bf16), expert-major
+__device__ __forceinline__ void unit_of(const FfnBatch &b, const Plan &p, bool quant, int i, int &j, int &s) {
+  for (j = 0; j < b.n; ++j) {
+    if ((b.e[j].bits != 16) != quant) continue;
+    if (i < p.ep[j].units) break;
+    i -= p.ep[j].units;
   }
-  int ts = tiles, is = I;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, ts, o), c = __shfl_up_sync(0xffffffffu, is, o);
-    if (lane >= o) ts += a, is += c;
-  }
-  if (lane < b.n) {
-    p.tile_off[lane] = ts - tiles;
-    p.rows_pt[lane] = R;
-    p.lay_off[lane] = is - I;
-    p.colsB[lane] = colsB;
-    p.ktiles[lane] = kt;
-  }
-  if (lane == b.n - 1) {
-    p.tile_off[b.n] = ts;
-    p.lay_off[b.n] = is;
-    p.n_a = ts;
-  }
+  s = i;
+}
+
+// Start of CTA c's bf16 range in weighted bytes: CTAs c < r carry q+1
+// quantized units (round-robin), the others q; each then takes bf16 work up to
+// the common target.  One expression with explicit roundings, evaluated the same
+// way by every CTA, so neighbouring ranges meet exactly.
+__device__ __noinline__ float share_prefix(int c, int r, float sA, float sB) {
+  return c < r ? __fmul_rn((float)c, sA) : __fadd_rn(__fmul_rn((float)r, sA), __fmul_rn((float)(c - r), sB));
+}
+
+// Warp 0: the assignment in O(1) per CTA (every CTA derives the same one).
+// Quantized units go round-robin; bf16 units fill every CTA to the same
+// weighted byte count (quantized unit cost = the batch's average).
+__device__ void make_plan(const FfnBatch &b, Plan &p, int G, int c, int lane) {
+  if (lane < b.n) expert_plan(b.e[lane], b.H, p.ep[lane]);
+  __syncwarp();
   if (lane == 0) {
-    int RBB = (H + grid - 1) / grid;
-    RBB = RBB < 1 ? 1 : RBB;
-    p.RBB = RBB;
-    p.n_blk = (H + RBB - 1) / RBB;
+    int nq = 0, ns = 0;
+    float cq = 0.f, cs = 0.f;
+    for (int j = 0; j < b.n; ++j) {
+      if (b.e[j].bits != 16) nq += p.ep[j].units, cq += p.ep[j].units * p.ep[j].cost;
+      else ns += p.ep[j].units, cs = p.ep[j].cost;
+    }
+    const float avg = nq ? cq / nq : 0.f;
+    const int q = nq / G, r = nq % G;
+    const float target = (cq + cs * ns) / G;
+    const float sA = fmaxf(0.f, target - (q + 1) * avg), sB = fmaxf(0.f, target - q * avg);
+    const float all = share_prefix(G, r, sA, sB);
+    const float scale = all > 0.f ? (float)ns / all : 0.f;
+    p.nq = nq;
+    p.ns = ns;
+    p.q_first = c;
+    p.nq_mine = q + (c < r ? 1 : 0);
+    p.s_lo = c == 0 ? 0 : min(ns, (int)rintf(__fmul_rn(share_prefix(c, r, sA, sB), scale)));
+    p.s_hi = c == G - 1 ? ns : min(ns, (int)rintf(__fmul_rn(share_prefix(c + 1, r, sA, sB), scale)));
+    if (p.s_hi < p.s_lo) p.s_hi = p.s_lo;
   }
+  __syncwarp();
 }
 
-__device__ unsigned int g_grid_barrier = 0;
-
-// per-CTA phase timestamps of the last launch (globaltimer ns), diagnostics only
-__device__ unsigned long long g_k3_prof[160][8];
-// CTA 0 per-warp tile timeline of the last launch (clock64 cycles):
-//   producer (warp 0): [tile][empty-wait start, empty passed, copies issued]
-//   consumer warp w:   [tile][full-wait start, full passed, stage released]
-constexpr int kTraceTiles = 48;
-__device__ long long g_k3_trace[17][kTraceTiles][3];
-// CTA 0, consumer warp 1, first 8 phase-A rows: [row][after dots, after warp sums, after store]
-__device__ long long g_k3_sub[8][4];
-#define K3_TRACE(w, t, slot) \
-  do { if (blockIdx.x == 0 && lane == 0 && (t) < kTraceTiles) g_k3_trace[w][t][slot] = clock64(); } while (0)
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// All CTAs are co-resident (grid = #SMs, one CTA per SM); the counter is never
-// reset: each launch waits for the next multiple of gridDim.x.
-__device__ __forceinline__ void grid_barrier() {
-  __threadfence();
-  const unsigned int old = atomicAdd(&g_grid_barrier, 1u);
-  const unsigned int target = (old / gridDim.x + 1u) * gridDim.x;
-  unsigned int v;
-  do {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&g_grid_barrier) : "memory");
-  } while ((int)(v - target) < 0);
+// The k-th unit of this CTA's sequence: quantized and bf16 units interleaved
+// evenly (compute-heavy and streaming units overlap in the ring).
+__device__ __forceinline__ void my_unit(const FfnBatch &b, const Plan &p, int G, int k, int &j, int &s) {
+  const int nq = p.nq_mine, ns = p.s_hi - p.s_lo, m = nq + ns;
+  // quantized unit number floor((k+1)*nq/m) - 1 sits at position k iff the count steps
+  const int before = (int)((long long)k * nq / m), after = (int)((long long)(k + 1) * nq / m);
+  if (after > before) unit_of(b, p, true, p.q_first + before * G, j, s);
+  else unit_of(b, p, false, p.s_lo + (k - before), j, s);
 }
 
 // x laid out for every width: slot s (chunk width cols = 8, 16, 32, 64
@@ -403,161 +424,165 @@ __device__ __forceinline__ void up_pair(const uint8_t *__restrict__ tile, int R,
   }
 }
 
-// Phase B: unit (c, h) of a tile -- words [h*U, h*U+U) of 16-byte chunk c
-// (global chunk cg of expert j's activation layout `at`, nchI chunks per
-// activation quad row) -- for MR rows of the tile, row[i] = 4 m_i + w4,
-// valid[i] = row exists; out[i] = w_j * dot(row[i]).  Quantized tiles with few
-// chunks per row use U = 2 or 1 so that the units still cover all 3 chunk groups.
-template <int BITS, int MR, int U>
-__device__ __forceinline__ void down_chunk(const uint8_t *tile, int nr, int nc, int c, int h,
-                                           const float4 *__restrict__ at, int nchI, int cg, const int (&row)[MR],
-                                           int valid, float wj, float (&out)[MR]) {
-  const int rowb = nc * BITS / 8;
-  uint4 q[MR];
-#pragma unroll
-  for (int i = 0; i < MR; ++i) {
-    const uint8_t *src = tile + row[i] * rowb + c * 16 + h * 4 * U;
-    if (!(valid >> i & 1)) q[i] = make_uint4(0, 0, 0, 0);
-    else if constexpr (U == 4) q[i] = *reinterpret_cast<const uint4 *>(src);
-    else if constexpr (U == 2) {
-      const uint2 t = *reinterpret_cast<const uint2 *>(src);
-      q[i] = make_uint4(t.x, t.y, 0, 0);
-    } else q[i] = make_uint4(*reinterpret_cast<const uint32_t *>(src), 0, 0, 0);
-  }
-  float2 p[MR][2];
-#pragma unroll
-  for (int i = 0; i < MR; ++i) p[i][0] = p[i][1] = make_float2(0.f, 0.f);
+// W-pieces cover whole 96-row blocks (12 consumer warps x 8 row quads),
+// B blocks per piece (compile time per format and H); a piece's last block may
+// be partial.  Row h0 + 96 b + 8 cw + rq belongs to warp cw, lanes 4 rq .. +3.
+template <int BITS, int HT>
+__host__ __device__ constexpr int w2_blocks() {
+  constexpr int rows = kStageBytes / (BITS == 16 ? kW2SlabBf16 * 2 : kW2SlabQuant * BITS / 8 + 8);
+  constexpr int per = BITS == 16 ? kRowsPerIterBf : kRowsPerIter;
+  // expert_plan: a piece is the whole of H when one stage holds it (bf16 slabs at
+  // H = 2048), else floor(rows / per) whole blocks; HT = 0 (any H): enough for both
+  if constexpr (HT == 0) return (rows + per - 1) / per;
+  else return rows >= HT ? (HT + per - 1) / per : rows / per;
+}
+
+// One W-piece: slab rows [h0, h0+nh) of W2_j against the unit's activations
+// aj[C] (w_j folded in).  Each lane first forms its columns' share of its B
+// rows in registers (a lane covers 16 columns of a quantized slab, its 16
+// activations in registers, or 2 of a bf16 slab), then the four lanes of a row
+// are summed in a fixed order and added to the CTA's partial y (one owner per
+// row, pieces in stage order: deterministic).  Out-of-range rows of the last
+// block read row 0 and are masked by a select, so the loop has no branches.
+template <int BITS, int B>
+__device__ __forceinline__ void w2_piece(const uint8_t *__restrict__ tile, int h0, int nh,
+                                         const float *__restrict__ aj, int cw, int lane, float *__restrict__ ysm) {
   if constexpr (BITS == 16) {
-    static_assert(U == 4, "bf16 tiles use whole chunks");
-    const float4 x0 = at[cg], x1 = at[nchI + cg];
+    // bf16 slab rows are 16 bytes: one lane per row (row h0 + 384 b + 32 cw + lane)
+    // with the unit's 8 activations in registers; its own accumulator row set
+    const float4 av0 = reinterpret_cast<const float4 *>(aj)[0], av1 = reinterpret_cast<const float4 *>(aj)[1];
+    float r[B];
 #pragma unroll
-    for (int i = 0; i < MR; ++i) {
-      p[i][0] = bf_dot(q[i].x, lo2(x0), p[i][0]);
-      p[i][1] = bf_dot(q[i].y, hi2(x0), p[i][1]);
-      p[i][0] = bf_dot(q[i].z, lo2(x1), p[i][0]);
-      p[i][1] = bf_dot(q[i].w, hi2(x1), p[i][1]);
+    for (int b = 0; b < B; ++b) {
+      const int hr = kRowsPerIterBf * b + 32 * cw + lane;
+      const bool ok = hr < nh;
+      const uint4 w = *reinterpret_cast<const uint4 *>(tile + (ok ? hr : 0) * 16);
+      float2 p0 = bf_dot(w.x, make_float2(av0.x, av0.y), make_float2(0.f, 0.f));
+      float2 p1 = bf_dot(w.y, make_float2(av0.z, av0.w), make_float2(0.f, 0.f));
+      p0 = bf_dot(w.z, make_float2(av1.x, av1.y), p0);
+      p1 = bf_dot(w.w, make_float2(av1.z, av1.w), p1);
+      r[b] = ok ? (p0.x + p0.y) + (p1.x + p1.y) : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < MR; ++i) out[i] = wj * ((p[i][0].x + p[i][0].y) + (p[i][1].x + p[i][1].y));
+    for (int b = 0; b < B; ++b) {
+      const int hr = kRowsPerIterBf * b + 32 * cw + lane;
+      if (hr < nh) ysm[h0 + hr] += r[b];
+    }
   } else {
-    constexpr int qpw = 32 / BITS / 4;
-    float2 sa = make_float2(0.f, 0.f);
-    float4 xv[4];
-#define FATE_WORD(WI)                                                      \
-  if constexpr ((WI) < U) {                                                \
-    _Pragma("unroll") for (int qi = 0; qi < qpw; ++qi) {                   \
-      xv[qi] = at[((h * U + (WI)) * qpw + qi) * nchI + cg];                \
-      sa = fadd2(sa, BITS == 4 ? unscale4(xv[qi]) : BITS == 2 ? unscale2(xv[qi], qi & 1)  \
-                                                   : fadd2(lo2(xv[qi]), hi2(xv[qi])));               \
-    }                                                                      \
-    _Pragma("unroll") for (int i = 0; i < MR; ++i) word_dot<BITS>(word<WI>(q[i]), xv, p[i][0], p[i][1]); \
-  }
-    FATE_WORD(0) FATE_WORD(1) FATE_WORD(2) FATE_WORD(3)
-#undef FATE_WORD
-    const float xsum = sa.x + sa.y;
-    const int szr = nc / 8;  // bytes of (scale, zero) pairs per row
-    const int grp = c / (kGroup / (128 / BITS));
+  const int rq = lane >> 2, sub = lane & 3;
+  const int own = 8 * cw + rq;
+  float r[B];
+  {
+    constexpr int wrb = kW2SlabQuant * BITS / 8;  // 16 / 32 / 64 bytes per slab row
+    constexpr int wpl = wrb / 16;                 // 32-bit code words per lane (1, 2, 4)
+    // the lane's 16 activations, prescaled for in-place code extraction (exact powers of two)
+    float4 xa[4];
+    float asum = 0.f;
 #pragma unroll
-    for (int i = 0; i < MR; ++i) {
-      const float2 z = (valid >> i & 1) ? reinterpret_cast<const float2 *>(tile + nr * rowb + row[i] * szr)[grp]
-                                        : make_float2(0.f, 0.f);
-      const float s = (p[i][0].x + p[i][0].y) + (p[i][1].x + p[i][1].y);
-      out[i] = wj * fmaf(z.x, s, z.y * xsum);
+    for (int q = 0; q < 4; ++q) {
+      float4 v = reinterpret_cast<const float4 *>(aj + 16 * sub)[q];
+      asum += (v.x + v.y) + (v.z + v.w);
+      if constexpr (BITS == 4) {
+        v.y *= 0.0625f, v.z *= 0.00390625f, v.w *= 0.000244140625f;
+      } else if constexpr (BITS == 2) {
+        const float bb = (q & 1) ? 0.00390625f : 1.0f;
+        v.x *= bb, v.y *= bb * 0.25f, v.z *= bb * 0.0625f, v.w *= bb * 0.015625f;
+      }
+      xa[q] = v;
+    }
+    asum += __shfl_xor_sync(0xffffffffu, asum, 1);
+    asum += __shfl_xor_sync(0xffffffffu, asum, 2);
+    const float zsum = sub == 0 ? asum : 0.f;  // the zero-point term once per row
+    const float2 *sz = reinterpret_cast<const float2 *>(tile + nh * wrb);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int hr = kRowsPerIter * b + own;
+      const bool ok = hr < nh;
+      const int hs = ok ? hr : 0;
+      const uint8_t *src = tile + hs * wrb + sub * (wrb / 4);
+      float2 p0 = make_float2(0.f, 0.f), p1 = p0;
+      if constexpr (wpl == 1) {
+        word_dot<BITS>(*reinterpret_cast<const uint32_t *>(src), xa, p0, p1);
+      } else if constexpr (wpl == 2) {
+        const uint2 w = *reinterpret_cast<const uint2 *>(src);
+        const float4 x0[4] = {xa[0], xa[1], xa[0], xa[1]}, x1[4] = {xa[2], xa[3], xa[2], xa[3]};
+        word_dot<BITS>(w.x, x0, p0, p1);
+        word_dot<BITS>(w.y, x1, p0, p1);
+      } else {
+        const uint4 w = *reinterpret_cast<const uint4 *>(src);
+        const float4 x0[4] = {xa[0], xa[0], xa[0], xa[0]}, x1[4] = {xa[1], xa[1], xa[1], xa[1]};
+        const float4 x2[4] = {xa[2], xa[2], xa[2], xa[2]}, x3[4] = {xa[3], xa[3], xa[3], xa[3]};
+        word_dot<BITS>(w.x, x0, p0, p1);
+        word_dot<BITS>(w.y, x1, p0, p1);
+        word_dot<BITS>(w.z, x2, p0, p1);
+        word_dot<BITS>(w.w, x3, p0, p1);
+      }
+      const float2 z = sz[hs];
+      r[b] = ok ? fmaf(z.x, (p0.x + p0.y) + (p1.x + p1.y), z.y * zsum) : 0.f;
     }
   }
-}
-
-// Rows of a phase B tile owned by consumer warp cw (12 warps): with 3 chunk
-// groups (G = 3) warp cw takes chunk group cw / 4 and rows r = 4m + cw % 4
-// (m = 0..3); with one group (G = 1, at most 32 units per row) it takes rows
-// cw and cw + 12.  Either way r = 4m + (cw & 3), so every thread's rows stay in
-// acc[m] for the whole sub-block whatever the tile's chunk-group count.
-template <int BITS, int MR, int U>
-__device__ __forceinline__ void down_tile(const uint8_t *tile, int nr, int nc, int c, int h,
-                                          const float4 *__restrict__ at, int nchI, int cg, int cw, float wj,
-                                          float (&acc)[4]) {
-  int m[MR], row[MR], valid = 0;
 #pragma unroll
-  for (int i = 0; i < MR; ++i) {
-    m[i] = MR == 4 ? i : (cw >> 2) + 3 * i;
-    row[i] = 4 * m[i] + (cw & 3);
-    if (row[i] < nr) valid |= 1 << i;
+  for (int b = 0; b < B; ++b) {
+    r[b] += __shfl_xor_sync(0xffffffffu, r[b], 1);
+    r[b] += __shfl_xor_sync(0xffffffffu, r[b], 2);
   }
-  float out[MR];
-  down_chunk<BITS, MR, U>(tile, nr, nc, c, h, at, nchI, cg, row, valid, wj, out);
+  if (sub == 0) {
 #pragma unroll
-  for (int i = 0; i < MR; ++i) {
-    if constexpr (MR == 4) {
-      acc[i] += out[i];
-    } else {
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm) acc[mm] += (m[i] == mm && (valid >> i & 1)) ? out[i] : 0.f;
+    for (int b = 0; b < B; ++b) {
+      const int hr = kRowsPerIter * b + own;
+      if (hr < nh) ysm[h0 + hr] += r[b];
     }
   }
-}
-
-template <int BITS, int U>
-__device__ __forceinline__ void down_tile_units(const TileMeta &tm, const uint8_t *tile, const FfnExpert &ex,
-                                                const float *al_j, int cw, int lane, int nch, float (&acc)[4]) {
-  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;  // columns per 16-byte chunk
-  const int nunits = nch * (4 / U);
-  const bool g3 = nunits > 32;
-  const int u = lane + (g3 ? 32 * (cw >> 2) : 0);
-  if (u >= nunits) return;
-  const int c = u / (4 / U), h = u % (4 / U);
-  const float4 *at = reinterpret_cast<const float4 *>(al_j);
-  const int nchI = ex.I / cols, cg = tm.k0 / cols + c;
-  if (g3) down_tile<BITS, 4, U>(tile, tm.nr, tm.nc, c, h, at, nchI, cg, cw, ex.weight, acc);
-  else down_tile<BITS, 2, U>(tile, tm.nr, tm.nc, c, h, at, nchI, cg, cw, ex.weight, acc);
-}
-
-// One phase B tile: the 12 consumer warps split the tile's units (chunks, or
-// half / quarter chunks of quantized rows with <= 48 / 24 chunks) into G groups
-// of 32 lanes (G = 1 or 3) and its rows into 12 / G residue classes.
-template <int BITS>
-__device__ __forceinline__ void down_tile_bits(const TileMeta &tm, const uint8_t *tile, const FfnExpert &ex,
-                                               const float *al_j, int cw, int lane, float (&acc)[4]) {
-  constexpr int cols = BITS == 16 ? 8 : 128 / BITS;
-  const int nch = tm.nc / cols;
-  if constexpr (BITS == 16) {
-    down_tile_units<16, 4>(tm, tile, ex, al_j, cw, lane, nch, acc);
-  } else {
-    if (nch > 48) down_tile_units<BITS, 4>(tm, tile, ex, al_j, cw, lane, nch, acc);
-    else if (nch > 24) down_tile_units<BITS, 2>(tm, tile, ex, al_j, cw, lane, nch, acc);
-    else down_tile_units<BITS, 1>(tm, tile, ex, al_j, cw, lane, nch, acc);
   }
 }
 
-// One launch per decode step:
-//   phase A  gate+up rows: a = silu(W1 x) * (W3 x).  Tiles go round-robin
-//            over the CTAs; consumer warp w takes the rows of tile k whose
-//            running index is w mod 12, so the rows of consecutive tiles land
-//            on different warps; a goes straight into the chunk-transposed layout of its
-//            expert (alay, global);
-//   barrier  grid-wide (all CTAs resident) so every activation is visible;
-//   phase B  each CTA owns a block of output rows (sub-blocks of <= 16) and
-//            streams column ranges of those rows of W2 of every expert; the
-//            12 consumer warps split the columns (chunk groups) and rows
-//            (r = 4m + w%4), accumulating w_j * dot in registers across all
-//            tiles, then one fixed-order reduction per row: y is deterministic.
-// The producers never wait for the barrier: W2 tiles are in flight while
-// phase A drains.
+// Co-residency is guaranteed by the cooperative launch (grid = #SMs, one CTA
+// per SM).  The counter belongs to the caller's scratch (one per engine) and is
+// never reset: each launch waits for the next multiple of gridDim.x.
+__device__ __forceinline__ void grid_barrier(unsigned int *ctr) {
+  __threadfence();
+  const unsigned int old = atomicAdd(ctr, 1u);
+  const unsigned int target = (old / gridDim.x + 1u) * gridDim.x;
+  unsigned int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  } while ((int)(v - target) < 0);
+}
+
+constexpr int kMaxGrid = 192;
+
+// Profiling builds only (-DFATE_PROF): per-CTA phase stamps (globaltimer ns) of
+// the last launch and CTA 0's per-stage consumer timeline (warp 4, lane 0).
+#ifdef FATE_PROF
+__device__ unsigned long long g_k3_prof[kMaxGrid][8];
+__device__ unsigned long long g_k3_stage[256][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K3_PROF(i) (g_k3_prof[blockIdx.x][i] = gtime())
+#define K3_STAGE(k, i, v) \
+  do { if (blockIdx.x == 0 && ctid == 0 && (k) < 256) g_k3_stage[k][i] = (v); } while (0)
+#else
+#define K3_PROF(i) ((void)0)
+#define K3_STAGE(k, i, v) ((void)0)
+#endif
+
 template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
-                                                          const float4 *__restrict__ xlay, float *__restrict__ alay,
-                                                          float *__restrict__ y, unsigned long long *bytes_stat,
-                                                          int stages, int nprod) {
+                                                          const float4 *__restrict__ xlay, float *__restrict__ part,
+                                                          unsigned int *__restrict__ bar, float *__restrict__ y,
+                                                          unsigned long long *bytes_stat, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FfnBatch batch;
   __shared__ Plan plan;
   __shared__ Ring ring;
   __shared__ TileMeta meta[kMaxStages];
-  __shared__ __align__(8) uint64_t x_bar, act_bar[kMaxFfnExperts];
-  __shared__ float part[kSubRows][3];
+  __shared__ __align__(8) uint64_t x_bar, act_bar[kActBufs];
+  __shared__ __align__(16) float a_sm[kActBufs][kW2SlabQuant];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned long long *prof = g_k3_prof[blockIdx.x < 160 ? blockIdx.x : 159];
-  if (blockIdx.x == 0)
-    for (int i = tid; i < 17 * kTraceTiles * 3; i += kThreads) (&g_k3_trace[0][0][0])[i] = 0;
+  const int G = gridDim.x;
   if (warp == 0) {
     // warp 0: batch copy with 16-byte loads, the plan, the barriers
     const int4 *src = reinterpret_cast<const int4 *>(batch_p);
@@ -567,29 +592,32 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     if (lane < batch.n && batch.e[lane].bits == 0)
       batch.e[lane].bits = reinterpret_cast<const ExpertHeader *>(batch.e[lane].buf)->bits;
     __syncwarp();
-    make_plan_warp(batch, plan, gridDim.x, lane);
     if (lane == 0) {
-      prof[0] = gtime();
       for (int s = 0; s < stages; ++s) {
         mbar_init(&ring.full[s], 1);
         mbar_init(&ring.empty[s], kConsumers);
       }
       mbar_init(&x_bar, 1);
-      for (int j = 0; j < batch.n; ++j) mbar_init(&act_bar[j], 1);
+      for (int b = 0; b < kActBufs; ++b) mbar_init(&act_bar[b], kConsumers);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (lane == 0) K3_PROF(0);
+    make_plan(batch, plan, G, blockIdx.x, lane);
+    if (lane == 0) K3_PROF(1);
   }
   __syncthreads();
   const int H = HT ? HT : batch.H;
   const int lay_stride = H / 4 + H / 32;
   uint8_t *ring_buf = smem;
-  float4 *xl = reinterpret_cast<float4 *>(smem + (size_t)stages * kStageBytes);  // x layouts (phase A)
-  float *al = reinterpret_cast<float *>(xl);                                      // activation layouts (phase B)
+  float4 *xl = reinterpret_cast<float4 *>(smem + (size_t)stages * kStageBytes);  // x layouts of the four widths
+  float *ysm = reinterpret_cast<float *>(xl + 4 * lay_stride);                  // partial y[H], quantized W2 rows
+  float *ysb = ysm + H;                                                          // partial y[H], bf16 W2 rows
+  const int n_units = plan.nq_mine + (plan.s_hi - plan.s_lo);
   if (warp < kProducers) {
-    // ================= producer warps: tile g of the stage sequence (phase A
-    // tiles, end marker, phase B tiles) belongs to producer g % kProducers, so
-    // the ~0.1 us issue latency of each bulk copy overlaps across warps.  The
-    // ring has more stages than producers, so an empty-barrier parity never aliases.
+    // ================= producers: stage g of the sequence (A- and W-pieces of
+    // every unit, then the end marker) belongs to producer g % kProducers, so
+    // the issue latency of the bulk copies overlaps across warps.  The ring has
+    // more stages than producers, so an empty-barrier parity never aliases.
     const int pw = warp;
     if (pw == 0 && lane == 0) {
       const uint32_t xbytes = (uint32_t)(4 * lay_stride * 16);
@@ -601,282 +629,240 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
         atomicAdd(bytes_stat, bytes);
       }
     }
-    // active producers: fewer than the ring's stages (parity safety)
-    const int np = nprod < stages - 1 ? nprod : stages - 1;
+    const int np = kProducers < stages - 1 ? kProducers : stages - 1;
     if (pw >= np) return;
-    int stage = 0, ti = 0;  // ti = position in the stage sequence
-    uint32_t phase = 0;
-    auto mine = [&]() -> bool {
-      stage = ti % stages;
-      phase = (uint32_t)(ti / stages) & 1u;
-      return ti % np == pw;
+    int st_ = 0, own_ = 0;  // stage of the next tile, its producer (tile index mod np)
+    uint32_t ph_ = 0;
+    auto begin = [&](int &stage, uint32_t &phase) -> bool {
+      stage = st_;
+      phase = ph_;
+      const bool mine = own_ == pw;
+      if (++st_ == stages) st_ = 0, ph_ ^= 1u;
+      if (++own_ == np) own_ = 0;
+      if (mine) mbar_wait(&ring.empty[stage], phase ^ 1);
+      return mine;
     };
-    // one phase A tile (or the end marker); returns true at the end
-    auto step_a = [&](int t) -> bool {
-      if (!mine()) {
-        ++ti;
-        return t >= plan.n_a;
-      }
-      K3_TRACE(0, ti, 0);
-      mbar_wait(&ring.empty[stage], phase ^ 1);
-      const bool end = t >= plan.n_a;
-      if (end) {
-        if (lane == 0) {
-          meta[stage].j = -1;
-          mbar_arrive(&ring.full[stage]);
-        }
-      } else {
-        int j = 0;
-        while (t >= plan.tile_off[j + 1]) ++j;
-        const FfnExpert &ex = batch.e[j];
-        const int bits = ex.bits;
-        const int R = plan.rows_pt[j];
-        const int r0 = (t - plan.tile_off[j]) * R, nr = min(R, ex.I - r0);
-        const uint32_t rb = (uint32_t)H * bits / 8, szb = bits == 16 ? 0u : (uint32_t)H / 8;
-        const uint32_t cb = nr * rb, sb = nr * szb;
+    // stage sequence: A(0) A(1) W(0) A(2) W(1) ... A(m-1) W(m-2) W(m-1)
+    auto issue_w = [&](int k, int j, int s) {
+      const FfnExpert &ex = batch.e[j];
+      const ExpertPlan &ep = plan.ep[j];
+      const int bits = ex.bits;
+      const Layout Lo = make_layout(H, ex.I, bits);
+      const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
+      const uint32_t wrb = (uint32_t)w2_row_bytes(bits), wsz = (uint32_t)w2_sz_bytes(bits);
+      for (int w = 0; w < ep.npw; ++w) {
+        int stage;
+        uint32_t phase;
+        if (!begin(stage, phase)) continue;
+        const int h0 = w * ep.rw, nh = min(ep.rw, H - h0);
+        const int64_t row = (int64_t)s * H + h0;
         uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
         if (lane == 0) {
-          meta[stage].j = j;
-          meta[stage].r0 = r0;
-          meta[stage].nr = nr;
-          mbar_expect_tx(&ring.full[stage], 2 * (cb + sb));
+          meta[stage] = TileMeta{1, j, s, h0, nh, w == 0, k % kActBufs, (k / kActBufs) & 1};
+          mbar_expect_tx(&ring.full[stage], (uint32_t)nh * (wrb + wsz));
+          bulk_g2s(dst, p + Lo.c2 + row * wrb, nh * wrb, &ring.full[stage]);
+        }
+        if (lane == 1 && wsz) bulk_g2s(dst + nh * wrb, p + Lo.s2 + row * wsz, nh * wsz, &ring.full[stage]);
+      }
+    };
+    int pj = -1, ps = 0;
+    for (int k = 0; k < n_units; ++k) {
+      int j, s;
+      my_unit(batch, plan, G, k, j, s);
+      const FfnExpert &ex = batch.e[j];
+      const ExpertPlan &ep = plan.ep[j];
+      const int bits = ex.bits;
+      const Layout Lo = make_layout(H, ex.I, bits);
+      const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
+      const uint32_t rb = (uint32_t)H * bits / 8, szb = bits == 16 ? 0u : (uint32_t)H / 8;
+      for (int a = 0; a < ep.npa; ++a) {
+        int stage;
+        uint32_t phase;
+        if (!begin(stage, phase)) continue;
+        const int r0 = a * ep.ra, nr = min(ep.ra, ep.C - r0);
+        const int64_t row = (int64_t)s * ep.C + r0;
+        uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
+        if (lane == 0) {
+          meta[stage] = TileMeta{0, j, s, r0, nr, a == ep.npa - 1, k % kActBufs, (k / kActBufs) & 1};
+          mbar_expect_tx(&ring.full[stage], 2u * nr * (rb + szb));
         }
         __syncwarp();
-        K3_TRACE(0, ti, 1);
-        if (lane < (sb ? 4 : 2)) {
+        if (lane < (szb ? 4 : 2)) {
           // lanes 0..3: W1 codes, W3 codes, W1 (scale, zero), W3 (scale, zero)
-          const int64_t n = (int64_t)H * ex.I, cbytes = bits == 16 ? 2 * n : n * bits / 8;
-          const int64_t sbytes = n / kGroup * 8;
-          const int64_t src = lane == 0 ? (int64_t)r0 * rb
-                            : lane == 1 ? cbytes + (int64_t)r0 * rb
-                            : lane == 2 ? 3 * cbytes + (int64_t)r0 * szb
-                                        : 3 * cbytes + sbytes + (int64_t)r0 * szb;
-          const uint32_t off = lane == 0 ? 0u : lane == 1 ? R * rb : lane == 2 ? 2 * R * rb : 2 * R * rb + R * szb;
-          bulk_g2s(dst + off, ex.buf + FATE_HEADER_BYTES + src, lane < 2 ? cb : sb, &ring.full[stage]);
+          const int64_t src = lane == 0 ? Lo.c1 + row * rb : lane == 1 ? Lo.c3 + row * rb
+                            : lane == 2 ? Lo.s1 + row * szb : Lo.s3 + row * szb;
+          const uint32_t off = lane == 0 ? 0u : lane == 1 ? nr * rb : lane == 2 ? 2 * nr * rb : 2 * nr * rb + nr * szb;
+          bulk_g2s(dst + off, p + src, lane < 2 ? nr * rb : nr * szb, &ring.full[stage]);
         }
       }
-      K3_TRACE(0, ti, 2);
-      ++ti;
-      return end;
-    };
-    // static round-robin over the tile list (expert-major, so every CTA gets a
-    // proportional mix of each expert's format), walked alternately from both
-    // ends so compute-heavy quantized tiles interleave with bf16 streaming
-    // tiles; then the end marker
-    {
-      const int K = plan.n_a > (int)blockIdx.x ? (plan.n_a - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-      for (int i = 0; i < K; ++i) {
-        const int kk = (i & 1) ? K - 1 - (i >> 1) : (i >> 1);
-        step_a((int)blockIdx.x + kk * (int)gridDim.x);
-      }
-      step_a(plan.n_a);  // end marker
+      if (pj >= 0) issue_w(k - 1, pj, ps);
+      pj = j, ps = s;
     }
-    for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x) {
-      const int R0 = blk * plan.RBB, rows = min(plan.RBB, H - R0);
-      for (int s0 = 0; s0 < rows; s0 += kSubRows) {
-        const int nr = min(kSubRows, rows - s0), rs0 = R0 + s0;
-        // the sub-block's tiles (expert j, K-range kt), walked alternately from
-        // both ends of the expert-major list (routed quantized tiles interleave
-        // with the shared expert's bf16 tiles); the last one carries the flush
-        int total = 0;
-        for (int j = 0; j < batch.n; ++j) total += plan.ktiles[j];
-        for (int i = 0; i < total; ++i) {
-          int pos = (i & 1) ? total - 1 - (i >> 1) : (i >> 1), j = 0;
-          while (pos >= plan.ktiles[j]) pos -= plan.ktiles[j], ++j;
-          const int kt = pos;
-          const FfnExpert &ex = batch.e[j];
-          const int bits = ex.bits;
-          const Layout L = make_layout(H, ex.I, bits);
-          const int64_t rb = L.row_bytes_down, szb = sz_row_bytes(ex.I, bits);
-          const uint8_t *p = ex.buf + FATE_HEADER_BYTES;
-          if (!mine()) {
-            ++ti;
-          } else {
-            const int k0 = kt * plan.colsB[j], nc = min(plan.colsB[j], ex.I - k0);
-            const uint32_t cb = (uint32_t)nc * bits / 8, sb = bits == 16 ? 0u : (uint32_t)nc / 8;
-            K3_TRACE(0, ti, 0);
-            mbar_wait(&ring.empty[stage], phase ^ 1);
-            uint8_t *dst = ring_buf + (size_t)stage * kStageBytes;
-            if (lane == 0) {
-              TileMeta &m = meta[stage];
-              m.j = j;
-              m.r0 = rs0;
-              m.nr = nr;
-              m.k0 = k0;
-              m.nc = nc;
-              m.flush = i == total - 1;
-              mbar_expect_tx(&ring.full[stage], (uint32_t)nr * (cb + sb));
-            }
-            __syncwarp();
-            K3_TRACE(0, ti, 1);
-            if (ex.layout == 1) {
-              // bf16 W2 in column slabs (kSlabCols == this K-range): the tile's rows are contiguous
-              if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)H * k0 * 2 + (int64_t)rs0 * nc * 2,
-                                      nr * cb, &ring.full[stage]);
-            } else if (nc == ex.I) {
-              // whole rows: the tile's rows are contiguous in the buffer, one copy
-              // for the codes and one for the (scale, zero) pairs
-              if (lane == 0) bulk_g2s(dst, p + L.c2 + (int64_t)rs0 * rb, nr * cb, &ring.full[stage]);
-              if (lane == 1 && sb) bulk_g2s(dst + nr * cb, p + L.s2 + (int64_t)rs0 * szb, nr * sb, &ring.full[stage]);
-            } else if (lane < nr) {
-              const int64_t r = rs0 + lane;
-              bulk_g2s(dst + lane * cb, p + L.c2 + r * rb + (int64_t)k0 * bits / 8, cb, &ring.full[stage]);
-              if (sb) bulk_g2s(dst + nr * cb + lane * sb, p + L.s2 + r * szb + k0 / 8, sb, &ring.full[stage]);
-            }
-            K3_TRACE(0, ti, 2);
-            ++ti;
-          }
-        }
+    if (pj >= 0) issue_w(n_units - 1, pj, ps);
+    {  // end marker
+      int stage;
+      uint32_t phase;
+      if (begin(stage, phase) && lane == 0) {
+        meta[stage].kind = 2;
+        mbar_arrive(&ring.full[stage]);
       }
     }
-    if (lane == 0 && pw == 0) prof[7] = gtime();
     return;
   }
   // ================= consumers
   const int ctid = tid - 32 * kProducers, cw = warp - kProducers;
-  if (ctid == 0) prof[1] = gtime();
+  // this CTA's partial y, one array per row-ownership pattern (quantized slabs: 4 lanes
+  // per row; bf16 slabs: one lane per row), so every row of each has a single writer
+  for (int i = ctid; i < 2 * H; i += 32 * kConsumers) ysm[i] = 0.f;
   mbar_wait(&x_bar, 0);  // x layouts landed
-  if (ctid == 0) prof[2] = gtime();
-  int stage = 0, k = 0, rot = 0;
+  if (ctid == 0) K3_PROF(2);
+  int stage = 0, rot = 0;
   uint32_t phase = 0;
-  for (;; ++k) {
-    K3_TRACE(cw + 1, k, 0);
+#ifdef FATE_PROF
+  int kk = 0;
+#endif
+  for (;;) {
+#ifdef FATE_PROF
+    K3_STAGE(kk, 0, gtime());
+#endif
     mbar_wait(&ring.full[stage], phase);
-    K3_TRACE(cw + 1, k, 1);
-    const int j = meta[stage].j;
-    if (j < 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ring.empty[stage]);
-      if (++stage == stages) stage = 0, phase ^= 1;
-      ++k;
-      break;
-    }
-    const int r0 = meta[stage].r0, nr = meta[stage].nr;
-    const FfnExpert &ex = batch.e[j];
-    const int bits = ex.bits, sl = bits_slot(bits);
-    const int R = plan.rows_pt[j];
-    const float4 *xt = xl + sl * lay_stride;
-    const float *xs = reinterpret_cast<const float *>(xl + sl * lay_stride + H / 4);
+    const TileMeta tm = meta[stage];
+#ifdef FATE_PROF
+    K3_STAGE(kk, 1, gtime());
+    K3_STAGE(kk, 3, (unsigned long long)(tm.kind * 1000000 + tm.j * 10000 + tm.nr));
+#endif
+    if (tm.kind == 2) break;
     const uint8_t *tile = ring_buf + (size_t)stage * kStageBytes;
-    // W2 chunk width of this expert (power of two): a[r] -> (r/cols, (r%cols)/4, r&3)
-    const int lc = bits == 16 ? 3 : bits == 8 ? 4 : bits == 4 ? 5 : 6;
-    float *aj = alay + plan.lay_off[j];
-    const int nch_a = ex.I >> lc;
-    int row0 = cw - rot;
-    if (row0 < 0) row0 += kConsumers;
-    for (int row = row0; row < nr; row += kConsumers) {
-      float u, v;
+    const FfnExpert &ex = batch.e[tm.j];
+    const int bits = ex.bits;
+    if (tm.kind == 0) {
+      // A-piece: consumer warp w takes the piece's rows whose running index is w mod 12
+      const int sl = bits == 16 ? 0 : bits == 8 ? 1 : bits == 4 ? 2 : 3;
+      const float4 *xt = xl + sl * lay_stride;
+      const float *xs = reinterpret_cast<const float *>(xl + sl * lay_stride + H / 4);
+      float *aj = a_sm[tm.ub];
+      int row = cw - rot;
+      if (row < 0) row += kConsumers;
+      for (; row < tm.nr; row += kConsumers) {
+        float u, v;
+        switch (bits) {
+          case 16: up_pair<16, HT>(tile, tm.nr, row, H, xt, xs, lane, u, v); break;
+          case 8: up_pair<8, HT>(tile, tm.nr, row, H, xt, xs, lane, u, v); break;
+          case 4: up_pair<4, HT>(tile, tm.nr, row, H, xt, xs, lane, u, v); break;
+          default: up_pair<2, HT>(tile, tm.nr, row, H, xt, xs, lane, u, v); break;
+        }
+        u = warp_sum(u);
+        v = warp_sum(v);
+        if (lane == 0) aj[tm.r0 + row] = ex.weight * (u / (1.0f + expf(-u)) * v);
+      }
+      rot = (rot + tm.nr) % kConsumers;
+      __syncwarp();
+      if (tm.flag && lane == 0) mbar_arrive(&act_bar[tm.ub]);  // this warp's rows of the unit are written
+    } else {
+      // W-piece: the unit's activations are complete once every consumer warp arrived
+      if (tm.flag) mbar_wait(&act_bar[tm.ub], (uint32_t)tm.par);
+      const float *aj = a_sm[tm.ub];
       switch (bits) {
-        case 16: up_pair<16, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
-        case 8: up_pair<8, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
-        case 4: up_pair<4, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
-        default: up_pair<2, HT>(tile, R, row, H, xt, xs, lane, u, v); break;
-      }
-      const long long c0 = clock64();
-      u = warp_sum(u);
-      v = warp_sum(v);
-      const long long c1 = clock64();
-      if (lane == 0) {
-        // straight into the chunk-transposed activation layout of phase B
-        const int r = r0 + row, c = r >> lc, m = (r & ((1 << lc) - 1)) >> 2;
-        float a = u / (1.0f + expf(-u)) * v;
-        if (bits == 4) a *= kInt4Prescale[r & 3];  // the INT4 / INT2 activation layouts are prescaled like x
-        else if (bits == 2) a *= kInt2Prescale[r & 7];
-        aj[(m * nch_a + c) * 4 + (r & 3)] = a;
-      }
-      if (blockIdx.x == 0 && cw == 0 && lane == 0 && k < 8) {
-        g_k3_sub[k][0] = c0;
-        g_k3_sub[k][1] = c1;
-        g_k3_sub[k][2] = clock64();
+        case 16: w2_piece<16, w2_blocks<16, HT>()>(tile, tm.r0, tm.nr, aj, cw, lane, ysb); break;
+        case 8: w2_piece<8, w2_blocks<8, HT>()>(tile, tm.r0, tm.nr, aj, cw, lane, ysm); break;
+        case 4: w2_piece<4, w2_blocks<4, HT>()>(tile, tm.r0, tm.nr, aj, cw, lane, ysm); break;
+        default: w2_piece<2, w2_blocks<2, HT>()>(tile, tm.r0, tm.nr, aj, cw, lane, ysm); break;
       }
     }
-    rot = (rot + nr) % kConsumers;
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[stage]);
-    K3_TRACE(cw + 1, k, 2);
+#ifdef FATE_PROF
+    K3_STAGE(kk, 2, gtime());
+    ++kk;
+#endif
     if (++stage == stages) stage = 0, phase ^= 1;
   }
-  // ---- every CTA's activations are complete and visible
+  // ---- partial y of this CTA -> global (the four lanes of a row summed in a
+  // fixed order); one grid barrier; CTA c sums its rows over the CTAs in order
+  if (ctid == 0) K3_PROF(3);
+  consumer_sync();
+  float *mine = part + (size_t)blockIdx.x * H;
+  for (int i = ctid; i < H; i += 32 * kConsumers) mine[i] = ysm[i] + ysb[i];
   consumer_sync();
   if (ctid == 0) {
-    prof[3] = gtime();
-    grid_barrier();
-    prof[4] = gtime();
-    // per-expert bulk copies of the activation layouts, in phase-B order
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int j = 0; j < batch.n; ++j) {
-      const uint32_t abytes = (uint32_t)(batch.e[j].I * 4);
-      mbar_expect_tx(&act_bar[j], abytes);
-      bulk_g2s(al + plan.lay_off[j], alay + plan.lay_off[j], abytes, &act_bar[j]);
-    }
+    K3_PROF(4);
+    grid_barrier(bar);
+    K3_PROF(5);
   }
-  // ---- phase B: tiles in producer order; flush = last tile of a row sub-block
-  const int w4 = cw & 3;  // this warp's rows are r = 4m + w4
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  bool first = true;
-  int subs_left = 0;  // row sub-blocks this CTA reduces (one flush each)
-  for (int blk = blockIdx.x; blk < plan.n_blk; blk += gridDim.x)
-    subs_left += (min(plan.RBB, H - blk * plan.RBB) + kSubRows - 1) / kSubRows;
-  while (subs_left > 0) {
-    K3_TRACE(cw + 1, k, 0);
-    mbar_wait(&ring.full[stage], phase);
-    K3_TRACE(cw + 1, k, 1);
-    const TileMeta tm = meta[stage];
-    const FfnExpert &ex = batch.e[tm.j];
-    mbar_wait(&act_bar[tm.j], 0);
-    if (first && ctid == 0) prof[5] = gtime();
-    first = false;
-    const uint8_t *tile = ring_buf + (size_t)stage * kStageBytes;
-    const float *al_j = al + plan.lay_off[tm.j];
-    switch (ex.bits) {
-      case 16: down_tile_bits<16>(tm, tile, ex, al_j, cw, lane, acc); break;
-      case 8: down_tile_bits<8>(tm, tile, ex, al_j, cw, lane, acc); break;
-      case 4: down_tile_bits<4>(tm, tile, ex, al_j, cw, lane, acc); break;
-      default: down_tile_bits<2>(tm, tile, ex, al_j, cw, lane, acc); break;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ring.empty[stage]);
-    K3_TRACE(cw + 1, k, 2);
-    ++k;
-    if (++stage == stages) stage = 0, phase ^= 1;
-    if (tm.flush) {
-      // fixed-order reduction: row r = 4m + w4 collects warps w4, w4 + 4, w4 + 8
+  consumer_sync();
+  // rows [r0, r0 + nrow) of y: thread (g, r) sums the CTAs c = g, g + ng, ... of row r,
+  // then the ng group sums are added in order (one global round trip)
+  const int RB = (H + G - 1) / G, r0 = blockIdx.x * RB, nrow = max(0, min(H, r0 + RB) - r0);
+  float *red = reinterpret_cast<float *>(ring_buf);  // the ring is idle now
+  if (nrow > 0) {
+    const int ng = (32 * kConsumers) / nrow;
+    const int g = ctid / nrow, r = ctid % nrow;
+    if (g < ng) {
+      constexpr int kPer = 8;
+      float acc = 0.f;
+      for (int c0 = g; c0 < G; c0 += kPer * ng) {
+        float v[kPer];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const float v = warp_sum(acc[m]);
-        if (lane == 0 && 4 * m + w4 < tm.nr) part[4 * m + w4][cw >> 2] = v;
-        acc[m] = 0.f;
+        for (int m = 0; m < kPer; ++m) {
+          const int c = c0 + m * ng;
+          v[m] = c < G ? __ldcg(part + (size_t)c * H + r0 + r) : 0.f;
+        }
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) acc += v[m];
       }
-      consumer_sync();
-      if (ctid < tm.nr) y[tm.r0 + ctid] = (part[ctid][0] + part[ctid][1]) + part[ctid][2];
-      consumer_sync();
-      --subs_left;
+      red[g * nrow + r] = acc;
+    }
+    consumer_sync();
+    if (ctid < nrow) {
+      float acc = 0.f;
+      for (int gg = 0; gg < ng; ++gg) acc += red[gg * nrow + ctid];
+      y[r0 + ctid] = acc;
     }
   }
-  if (ctid == 0) prof[6] = gtime();
+  if (ctid == 0) K3_PROF(6);
 }
 
-int g_num_sms = 0;
+struct DevInfo {
+  int sms = 0;
+  bool configured = false;
+};
+std::mutex g_dev_mu;
+DevInfo g_dev[64];
 
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!g_num_sms) g_num_sms = 148;
+cudaError_t configure_device(int dev) {
+  cudaError_t e = cudaSuccess;
+  const int dyn = (int)(kSmemLimit - 8192);
+  for (const void *f : {(const void *)ffn_kernel<0>, (const void *)ffn_kernel<2048>, (const void *)ffn_kernel<4096>}) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
-  return g_num_sms;
+  cudaFuncAttributes a;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, build_xlay_kernel);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(build_xlay_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+  return e;
 }
 
-// dynamic smem beyond the ring: max(x layouts of every width, activation
-// layouts of every expert with bf16-size chunk sums + the partial-sum table)
-size_t region_bytes(int H, int max_total_I) {
-  const size_t xb = (size_t)4 * (H / 4 + H / 32) * 16;  // x layouts of the four widths (phase A)
-  const size_t ab = (size_t)max_total_I * 4;             // activation layouts of every expert (phase B)
-  return xb > ab ? xb : ab;
+// per-device one-time setup (kernel attributes are per device context)
+cudaError_t device_info(int *sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_dev[dev].configured) {
+    e = configure_device(dev);
+    if (e != cudaSuccess) return e;
+    g_dev[dev].configured = true;
+  }
+  *sms = g_dev[dev].sms;
+  return cudaSuccess;
 }
 
-constexpr size_t kStaticReserve = 4096;  // static shared memory (batch, plan, barriers, partials)
+// dynamic smem beyond the ring: x layouts of the four widths + the partial y
+size_t region_bytes(int H) { return (size_t)4 * (H / 4 + H / 32) * 16 + (size_t)2 * H * 4; }
+
+constexpr size_t kStaticReserve = 8192;  // static shared memory (batch, plan, barriers, loads, activations)
 
 int stages_for(size_t extra) {
   int s = kMaxStages;
@@ -887,82 +873,83 @@ int stages_for(size_t extra) {
 }  // namespace
 
 cudaError_t ffn_preload() {
-  cudaFuncAttributes a;
-  cudaError_t e = cudaFuncGetAttributes(&a, build_xlay_kernel);
-  const int dyn = (int)(kSmemLimit - kStaticReserve);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(ffn_kernel<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-  for (const void *f : {(const void *)ffn_kernel<0>, (const void *)ffn_kernel<2048>, (const void *)ffn_kernel<4096>,
-                        (const void *)build_xlay_kernel})
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  return e;
+  int sms = 0;
+  return device_info(&sms);
 }
 
 size_t ffn_xlay_floats(int H) { return (size_t)4 * (H / 4 + H / 32) * 4; }
 
-size_t ffn_alay_floats(int max_total_I) { return (size_t)max_total_I + max_total_I / 8 + 4 * kMaxFfnExperts; }
+size_t ffn_scratch_bytes(int H) {
+  int sms = 0;
+  if (device_info(&sms) != cudaSuccess || sms < 1) sms = kMaxGrid;
+  return ((size_t)sms * H * 4 + 255) / 256 * 256 + 256;  // partials [sms][H] + the barrier word
+}
 
 cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s) {
   build_xlay_kernel<<<1, 512, H * sizeof(float), s>>>(x, H, reinterpret_cast<float4 *>(xlay));
   return cudaGetLastError();
 }
 
-cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
-                              int max_total_I, cudaStream_t s) {
-  return launch_ffn_decode_engine(batch_dev, xlay, alay, y_dev, H, max_total_I, nullptr, s);
+cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
+                              cudaStream_t s) {
+  return launch_ffn_decode_engine(batch_dev, xlay, scratch, y_dev, H, nullptr, s);
 }
 
-cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, float *alay, float *y_dev, int H,
-                                     int max_total_I, unsigned long long *bytes_stat, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = ffn_preload();
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  const int sms = num_sms();
-  const size_t extra = region_bytes(H, max_total_I);
+cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
+                                     unsigned long long *bytes_stat, cudaStream_t s) {
+  int sms = 0;
+  cudaError_t e = device_info(&sms);
+  if (e != cudaSuccess) return e;
+  if (sms > kMaxGrid) sms = kMaxGrid;
+  const size_t extra = region_bytes(H);
   const int st = stages_for(extra);
-  static const int nprod = [] {
-    const char *e = getenv("FATE_K3_PRODUCERS");  // tuning knob: producer warps actually issuing (1..4)
-    const int v = e ? atoi(e) : kProducers;
-    return v < 1 ? 1 : v > kProducers ? kProducers : v;
-  }();
   const size_t smem = (size_t)st * kStageBytes + extra;
   if (smem + kStaticReserve > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
-  // the grid barrier needs every CTA resident: one CTA per SM, grid = #SMs
+  float *part = reinterpret_cast<float *>(scratch);
+  unsigned int *bar = reinterpret_cast<unsigned int *>(reinterpret_cast<uint8_t *>(scratch) +
+                                                       ((size_t)sms * H * 4 + 255) / 256 * 256);
   const float4 *xl = reinterpret_cast<const float4 *>(xlay);
-  if (H == 2048)
-    ffn_kernel<2048><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
-  else if (H == 4096)
-    ffn_kernel<4096><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
-  else
-    ffn_kernel<0><<<sms, kThreads, smem, s>>>(batch_dev, xl, alay, y_dev, bytes_stat, st, nprod);
-  return cudaGetLastError();
+  // cooperative: every CTA resident (one per SM), which the final grid barrier needs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (H == 2048) return cudaLaunchKernelEx(&cfg, ffn_kernel<2048>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
+  if (H == 4096) return cudaLaunchKernelEx(&cfg, ffn_kernel<4096>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
+  return cudaLaunchKernelEx(&cfg, ffn_kernel<0>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
 }
 
 }  // namespace fate
 
-// Diagnostics: per-CTA phase timestamps of the last K3 launch, [160][8] ns.
+// Profiling builds (FATE_PROF=1): out_host[192*8] per-CTA stamps (ns) of the last
+// launch: start, plan, x landed, ring drained, partials written, barrier passed,
+// done; then out_host[192*8 + 256*4] CTA 0's per-stage [wait, full, released, tag].
 extern "C" int fate_k3_profile(uint64_t *out_host) {
-  if (cudaMemcpyFromSymbol(out_host + 160 * 8 + 17 * fate::kTraceTiles * 3, fate::g_k3_sub, sizeof(long long) * 32) !=
-      cudaSuccess)
-    return FATE_ECUDA;
-  if (cudaMemcpyFromSymbol(out_host + 160 * 8, fate::g_k3_trace, sizeof(long long) * 17 * fate::kTraceTiles * 3) !=
-      cudaSuccess)
-    return FATE_ECUDA;
-  if (cudaMemcpyFromSymbol(out_host, fate::g_k3_prof, sizeof(unsigned long long) * 160 * 8) != cudaSuccess) {
+#ifdef FATE_PROF
+  if (cudaMemcpyFromSymbol(out_host, fate::g_k3_prof, sizeof(unsigned long long) * fate::kMaxGrid * 8) != cudaSuccess ||
+      cudaMemcpyFromSymbol(out_host + fate::kMaxGrid * 8, fate::g_k3_stage, sizeof(unsigned long long) * 256 * 4) !=
+          cudaSuccess) {
     fate::set_error("fate_k3_profile: copy failed");
     return FATE_ECUDA;
   }
   return FATE_OK;
+#else
+  (void)out_host;
+  fate::set_error("fate_k3_profile: K3 phase stamps are compiled in only with FATE_PROF=1");
+  return FATE_EINVAL;
+#endif
 }
 
 extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *const *bufs, const float *weights,
                                float *scratch_dev, float *y_dev, void *stream) {
   using namespace fate;
-  if (n < 1 || n > kMaxFfnExperts || H < 128 || H % 128) {
+  if (n < 1 || n > kMaxFfnExperts || H < 128 || H % 128 || H > 4096) {
     set_error("fate_ffn_decode: bad arguments");
     return FATE_EINVAL;
   }
@@ -984,16 +971,19 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
   }
   b.total_I = off;
   FfnBatch *bd = nullptr;
-  float *xl = nullptr, *al = nullptr;
+  float *xl = nullptr;
+  void *sc = nullptr;
+  const size_t scb = ffn_scratch_bytes(H);
   FATE_CUDA(cudaMallocAsync(&bd, sizeof(FfnBatch), s));
   FATE_CUDA(cudaMallocAsync(&xl, ffn_xlay_floats(H) * sizeof(float), s));
-  FATE_CUDA(cudaMallocAsync(&al, ffn_alay_floats(off) * sizeof(float), s));
+  FATE_CUDA(cudaMallocAsync(&sc, scb, s));
+  FATE_CUDA(cudaMemsetAsync(sc, 0, scb, s));
   FATE_CUDA(cudaMemcpyAsync(bd, &b, sizeof(b), cudaMemcpyHostToDevice, s));
   FATE_CUDA(launch_build_xlay(x_dev, H, xl, s));
-  cudaError_t e = launch_ffn_decode(bd, xl, al, y_dev, H, off, s);
+  cudaError_t e = launch_ffn_decode(bd, xl, sc, y_dev, H, s);
   cudaFreeAsync(bd, s);
   cudaFreeAsync(xl, s);
-  cudaFreeAsync(al, s);
+  cudaFreeAsync(sc, s);
   FATE_CUDA(e);
   (void)scratch_dev;
   FATE_CUDA(cudaStreamSynchronize(s));  // b lives on this stack frame
@@ -1003,13 +993,13 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
 extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets, const uint8_t *const *bufs,
                                      const float *weights, float *y_dev, int iters, void *stream, float *ms_out) {
   using namespace fate;
-  if (n < 1 || n > kMaxFfnExperts || nsets < 1 || nsets > 64 || H < 128 || H % 128 || iters < 1 || !ms_out) {
+  if (n < 1 || n > kMaxFfnExperts || nsets < 1 || nsets > 64 || H < 128 || H % 128 || H > 4096 || iters < 1 ||
+      !ms_out) {
     set_error("fate_ffn_decode_timed: bad arguments");
     return FATE_EINVAL;
   }
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<FfnBatch> bs(nsets);
-  int max_off = 0;
   for (int q = 0; q < nsets; ++q) {
     FfnBatch &b = bs[q];
     b = FfnBatch{};
@@ -1028,22 +1018,23 @@ extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets
       off += h.I;
     }
     b.total_I = off;
-    max_off = off > max_off ? off : max_off;
   }
   FfnBatch *bd = nullptr;
-  float *xl = nullptr, *al = nullptr;
+  float *xl = nullptr;
+  void *sc = nullptr;
+  const size_t scb = ffn_scratch_bytes(H);
   FATE_CUDA(cudaMalloc(&bd, sizeof(FfnBatch) * nsets));
   FATE_CUDA(cudaMalloc(&xl, ffn_xlay_floats(H) * sizeof(float)));
-  FATE_CUDA(cudaMalloc(&al, ffn_alay_floats(max_off) * sizeof(float)));
+  FATE_CUDA(cudaMalloc(&sc, scb));
+  FATE_CUDA(cudaMemset(sc, 0, scb));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaError_t e = cudaMemcpyAsync(bd, bs.data(), sizeof(FfnBatch) * nsets, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = launch_build_xlay(x_dev, H, xl, s);
-  for (int i = 0; i < nsets && e == cudaSuccess; ++i) e = launch_ffn_decode(bd + i, xl, al, y_dev, H, max_off, s);
+  for (int i = 0; i < nsets && e == cudaSuccess; ++i) e = launch_ffn_decode(bd + i, xl, sc, y_dev, H, s);
   if (e == cudaSuccess) e = cudaEventRecord(e0, s);
-  for (int i = 0; i < iters && e == cudaSuccess; ++i)
-    e = launch_ffn_decode(bd + (i % nsets), xl, al, y_dev, H, max_off, s);
+  for (int i = 0; i < iters && e == cudaSuccess; ++i) e = launch_ffn_decode(bd + (i % nsets), xl, sc, y_dev, H, s);
   if (e == cudaSuccess) e = cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaEventSynchronize(e1);
   float ms = 0.f;
@@ -1053,7 +1044,7 @@ extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets
   cudaEventDestroy(e1);
   cudaFree(bd);
   cudaFree(xl);
-  cudaFree(al);
+  cudaFree(sc);
   FATE_CUDA(e);
   return FATE_OK;
 }

@@ -321,17 +321,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (mat < (UP ? 2 : 1)) {
         const int64_t grow = r0 + row;
         const uint8_t *codes = p + (UP ? (mat ? L.c3 : L.c1) : L.c2);
+        // W1 / W3 rows are row-major; W2 is slab-major (fate_internal.cuh): the K-step's
+        // 64 columns of row grow are slab k0/64 (quantized) or slabs k0/8 .. +7 (bf16)
         if (bits == 16) {
-          const uint8_t *src = codes + (grow * K + c.k0) * 2;
 #pragma unroll
-          for (int k8 = 0; k8 < 8; ++k8) cp16(st + mat * kTileBytes + chunk_off(row, k8, BM), src + 16 * k8, true);
+          for (int k8 = 0; k8 < 8; ++k8) {
+            const uint8_t *src = UP ? codes + (grow * K + c.k0 + 8 * k8) * 2
+                                    : codes + ((int64_t)(c.k0 / kW2SlabBf16 + k8) * H + grow) * (kW2SlabBf16 * 2);
+            cp16(st + mat * kTileBytes + chunk_off(row, k8, BM), src, true);
+          }
         } else {
           const uint8_t *sz = p + (UP ? (mat ? L.s3 : L.s1) : L.s2);
           const int units = bits / 2;  // 16-byte code units per 64-column row segment
-          const uint8_t *src = codes + (grow * K + c.k0) * bits / 8;
+          const int64_t seg = UP ? (grow * K + c.k0) / kGroup : (int64_t)(c.k0 / kW2SlabQuant) * H + grow;
+          const uint8_t *src = codes + seg * (kGroup * bits / 8);
           uint8_t *tl = st + mat * kTileBytes;
           for (int u = 0; u < units; ++u) cp16(tl + chunk_off(row, 4 + u, BM), src + 16 * u, true);
-          cp8(tl + chunk_off(row, 3, BM), sz + (grow * K + c.k0) / kGroup * 8);
+          cp8(tl + chunk_off(row, 3, BM), sz + seg * 8);
         }
       }
       uint8_t *xt = st + (UP ? 2 : 1) * kTileBytes;

@@ -111,6 +111,17 @@ __global__ void write_header_kernel(uint8_t *dst, int bits, int layer, int exper
   }
 }
 
+// W2 [H, I] row-major -> slab-major (fate_internal.cuh): element (h, c) to
+// ((c / C) * H + h) * C + c % C.  With C = 64 every 64-element group of the
+// permuted array is one row segment of one original group.
+__global__ void w2_slab_kernel(const float *__restrict__ w2, int H, int I, int C, float *__restrict__ out) {
+  const int64_t n = (int64_t)H * I;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / I, c = i % I;
+    out[((c / C) * H + h) * C + c % C] = w2[i];
+  }
+}
+
 int grid_for(int64_t work, int per_block) {
   int64_t g = (work + per_block - 1) / per_block;
   if (g > 148 * 32) g = 148 * 32;
@@ -208,12 +219,18 @@ extern "C" int fate_pack_expert(const float *w1_dev, const float *w3_dev, const 
   const int64_t n = (int64_t)H * I;
   write_header_kernel<<<1, 64, 0, s>>>(dst_dev, bits, layer, expert, H, I);
   FATE_CHECK_LAUNCH("write_header_kernel");
-  const float *src[3] = {w1_dev, w3_dev, w2_dev};
+  // W2 goes into the slab-major order first (64-column slabs = whole groups; bf16: 8 columns)
+  float *w2s = nullptr;
+  FATE_CUDA(cudaMallocAsync(&w2s, (size_t)n * sizeof(float), s));
+  w2_slab_kernel<<<grid_for(n, 256), 256, 0, s>>>(w2_dev, H, I, bits == 16 ? kW2SlabBf16 : kW2SlabQuant, w2s);
+  cudaError_t le = cudaGetLastError();
+  const float *src[3] = {w1_dev, w3_dev, w2s};
   const int64_t co[3] = {L.c1, L.c3, L.c2};
   const int64_t so[3] = {L.s1, L.s3, L.s2};
-  for (int j = 0; j < 3; ++j) {
-    FATE_CUDA(quant_pack_launch(src[j], n, bits, kGroup, p + co[j],
-                                bits == 16 ? nullptr : reinterpret_cast<float *>(p + so[j]), nullptr, nullptr, s));
-  }
+  for (int j = 0; j < 3 && le == cudaSuccess; ++j)
+    le = quant_pack_launch(src[j], n, bits, kGroup, p + co[j],
+                           bits == 16 ? nullptr : reinterpret_cast<float *>(p + so[j]), nullptr, nullptr, s);
+  cudaFreeAsync(w2s, s);
+  FATE_CUDA(le);
   return FATE_OK;
 }

@@ -147,12 +147,16 @@ def knobs_for(strategy: Strategy, plan: CachePlan, n: int):
 
     pol = strategy.prefetch_policy or PrefetchPolicy("topk")
     qp = strategy.quant_policy
-    # eap: co-activation predictor in K1 (pipeline.py:301-321), decode only
+    # a predictor exists only for fate / eap with a prefetch policy: build_decode_predictor
+    # returns None otherwise (pipeline.py:330-331), and simulate_prefill's use_cross /
+    # use_eap require the policy too (pipeline.py:563-564).  eap: co-activation
+    # predictor in K1 (pipeline.py:301-321)
+    predicts = strategy.kind in ("fate", "eap") and strategy.prefetch_policy is not None
     return StrategyKnobs(
-        use_predictor=strategy.kind in ("fate", "eap"), policy="eap" if strategy.kind == "eap" else pol.kind,
+        use_predictor=predicts, policy="eap" if strategy.kind == "eap" else pol.kind,
         percentile_q=pol.percentile_q, budget_n=n,
         cached_bits=plan.cached_bits, prefetch_bits=strategy.prefetch_bits(), ondemand_bits=strategy.ondemand_bits(),
-        prefill_use_predictor=strategy.kind in ("fate", "eap"), reorder_prefill=strategy.reorder_prefill,
+        prefill_use_predictor=predicts, reorder_prefill=strategy.reorder_prefill,
         p_int2=qp.p_int2 if qp else 0.0, prefill_ondemand_bits=strategy.ondemand_bits() if strategy.kind == "fate" else 16)
 
 
@@ -226,6 +230,21 @@ def _resident_counts(logs, caps, L):
     return out
 
 
+class RoutingMismatchWarning(UserWarning):
+    """The device's fp64 router disagreed with a trace record's ``chosen`` set."""
+
+
+def _warn_mismatch(stats: dict) -> None:
+    # the engine follows record.chosen for every cache decision (pipeline.py:422), as
+    # the reference does; a disagreement of the recomputed routing (imported real-model
+    # traces, or near-ties) only affects the FFN routing weights, so it is reported
+    n = int(stats.get("trace_mismatches", 0))
+    if n:
+        import warnings
+        warnings.warn(f"{n} step(s): the recomputed top-k differs from the trace's chosen set; cache decisions "
+                      "follow the trace", RoutingMismatchWarning, stacklevel=3)
+
+
 def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, timing: TimingModel, cfg: ModelConfig,
                       weights=None, cache: LayeredExpertCache | None = None, predictor=None,
                       collect_cache_events: bool = False, *, experts=None, shared_intermediate: int = 0,
@@ -256,6 +275,7 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     res = eng.decode(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev), tokens=toks,
                      want_logs=collect_cache_events or return_result == "logs")
     st = res.stats
+    _warn_mismatch(st)
     L = cfg.num_layers
     events = []
     stall = 0.0
@@ -317,6 +337,7 @@ def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timi
         eng.reset_eap()  # a fresh EapStats (pipeline.py:572-574)
     dev = torch.device("cuda", eng.device)
     Y, st, logs, step_ms, copies = eng.prefill(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev))
+    _warn_mismatch(st)
     events = []
     stall = 0.0
     for l, row in enumerate(step_ms):

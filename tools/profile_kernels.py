@@ -66,7 +66,7 @@ def k3sweep(iters: int):
     x = torch.randn(H, device="cuda")
     specs = {"bf16_shared": [(Is, 16)], "int4x4": [(I, 4)] * 4, "int2x4": [(I, 2)] * 4, "int8x4": [(I, 8)] * 4,
              "qwen_mix_int4": [(I, 4)] * 4 + [(Is, 16)], "qwen_mix_int2": [(I, 2)] * 3 + [(I, 4), (Is, 16)],
-             "int4x12": [(I, 4)] * 12}
+             "int4x12": [(I, 4)] * 12, "qwen_bench_mix": [(I, 2)] * 4 + [(Is, 16)]}
     out = {}
     only = os.environ.get("K3_ONLY")
     for name, spec in specs.items():
@@ -80,9 +80,44 @@ def k3sweep(iters: int):
         del sets
         torch.cuda.empty_cache()
         print(name, json.dumps(out[name]))
-        from paper_2502_12224_b200 import _lib
-        print_k3_trace(_lib)
     print(json.dumps(out))
+
+
+def k3prof(iters: int):
+    """Profiling build only (FATE_PROF=1): K3 phase stamps per CTA and CTA 0's
+    per-stage consumer timeline, for each K3_SPECS mix (default: the bench mix)."""
+    from paper_2502_12224_b200 import _lib
+    H, I, Is = 2048, 1408, 5632
+    g = torch.Generator(device="cuda").manual_seed(0)
+
+    def mk(I_, bits, H_=H):
+        w = [torch.randn(sh, generator=g, device="cuda") * 0.02 for sh in ((I_, H_), (I_, H_), (H_, I_))]
+        return ops.pack_expert(*w, bits)
+    specs = {"bf16_shared": [(Is, 16)], "int2x4": [(I, 2)] * 4, "qwen_bench_mix": [(I, 2)] * 4 + [(Is, 16)],
+             "int4x4": [(I, 4)] * 4}
+    want = os.environ.get("K3_SPECS", "qwen_bench_mix,bf16_shared,int2x4").split(",")
+    x = torch.randn(H, device="cuda")
+    for name in want:
+        spec = specs[name]
+        sets = [[mk(i, b) for i, b in spec] for _ in range(4)]
+        _, ms = ops.ffn_decode_timed(x, sets, [0.1] * len(spec), iters)
+        buf = np.zeros(192 * 8 + 256 * 4, dtype=np.uint64)
+        _lib.load().fate_k3_profile(buf.ctypes.data)
+        P = buf[:192 * 8].reshape(192, 8).astype(np.int64)
+        P = P[:148]
+        t0 = P[:, 0].min()
+        names = ["start", "plan", "x", "drained", "partials", "barrier", "done"]
+        print(f"== {name}: {ms * 1e3:.2f} us per launch")
+        for i, nm in enumerate(names):
+            v = (P[:, i] - t0) / 1e3
+            print(f"  {nm:9s} median {np.median(v):7.2f}  min {v.min():7.2f}  max {v.max():7.2f}  argmax {int(v.argmax())}")
+        S = buf[192 * 8:].reshape(256, 4).astype(np.int64)
+        n = int((S[:, 1] > 0).sum())
+        print("  CTA0 stages: [wait-start, full, released] us, tag (kind*1e6 + j*1e4 + rows)")
+        for k in range(min(n, 40)):
+            print(f"   {k:3d} {(S[k, 0] - t0) / 1e3:7.2f} {(S[k, 1] - t0) / 1e3:7.2f} {(S[k, 2] - t0) / 1e3:7.2f}  {S[k, 3]}")
+        del sets
+        torch.cuda.empty_cache()
 
 
 def make_layout_bytes(H, I, bits):
@@ -288,4 +323,4 @@ if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
     {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline,
-     "mixtral": mixtral}[mode](it)
+     "mixtral": mixtral, "k3prof": k3prof}[mode](it)
