@@ -32,3 +32,46 @@ def config_traces(name: str):
     dec, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=0, num_tokens=c["dec_tokens"], phase="decoding"))
     pre, _ = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=1, num_tokens=c["pre_tokens"], phase="prefill"), weights=w)
     return cfg, dec, pre, w
+
+
+@functools.lru_cache(maxsize=1)
+def golden_big() -> dict:
+    """Reference schedules at the measured configurations (tests/golden/make_golden_big.py)."""
+    import gzip
+    with gzip.open(os.path.join(GOLDEN_DIR, "golden_big.json.gz"), "rt") as fh:
+        return json.load(fh)
+
+
+@functools.lru_cache(maxsize=4)
+def big_traces(name: str):
+    """(cfg, traces..., gate weights) of a golden_big entry, regenerated with the
+    package's generator (pinned to the reference bytes by the dec/pre sha256)."""
+    from paper_2502_12224_b200 import core, gatesim
+    e = golden_big()[name]
+    s = e["shape"]
+    cfg = core.ModelConfig.from_shape(s["L"], s["E"], s["k"], s["H"], s["I"], s["Lb"])
+    if name == "qwen_bench":
+        dec, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=0, num_tokens=e["tokens"], phase="decoding"))
+        return cfg, dec, w
+    if name == "qwen_lod":
+        dec, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=0, num_tokens=e["tokens"], phase="decoding"))
+        return cfg, dec, w
+    if name == "dsk_prefill512":
+        pre, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=0, num_tokens=e["pre_tokens"], phase="prefill"))
+        dec, _ = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=1, num_tokens=e["dec_tokens"], phase="decoding"),
+                                   weights=w)
+        return cfg, pre, dec, w
+    if name == "mixtral_sweep":
+        dec, w = gatesim.gen_trace(cfg, gatesim.GenConfig(seed=0, num_tokens=e["tokens"], phase="decoding"))
+        return cfg, dec, w
+    raise KeyError(name)
+
+
+def trace_sha(trace) -> str:
+    import hashlib
+    import tempfile
+    from paper_2502_12224_b200 import core
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "t.ndjson")
+        core.write_trace(trace, p)
+        return hashlib.sha256(open(p, "rb").read()).hexdigest()
