@@ -114,6 +114,20 @@ class _LayerView:
     def access(self, expert: int) -> bool:
         return self._c._engine_or_raise().access(self.layer, [int(expert)])[0]
 
+    def check_invariants(self) -> None:
+        """ArcState.check_invariants (cache.py:118-126) on the device state, plus
+        the engine's own invariant: the experts holding a buffer are exactly T1 u T2."""
+        st = self._state()
+        c = self.capacity
+        lists = [st["t1"], st["t2"], st["b1"], st["b2"]]
+        total = sum(len(l) for l in lists)
+        assert len(st["t1"]) + len(st["t2"]) <= c
+        assert len(st["t1"]) + len(st["b1"]) <= c
+        assert total <= 2 * c
+        assert len(set().union(*map(set, lists))) == total, "ARC lists must be disjoint"
+        assert 0.0 <= st["p"] <= c
+        assert self._c.engine.resident(self.layer) == set(st["t1"]) | set(st["t2"]), "slot map differs from ARC"
+
 
 class LayeredExpertCache:
     """Per-layer ARC caches sized by a CachePlan, state on the GPU (cache.py:182-204)."""

@@ -129,17 +129,35 @@ def transfer_budget(timing: TimingModel, bits: int) -> int:
 # engine plumbing
 
 _STORES: dict = {}
+_MAX_STORES = 2      # pinned host pools kept for reuse (each is GBs at model scale)
+_MAX_IDLE = 2        # idle engines kept per (store, plan, gates)
 
 
 def default_store(cfg: ModelConfig, bits, shared_intermediate: int = 0, seed: int = 0):
-    """Synthetic random-init experts for cfg, cached per (cfg, bits, shared, seed)."""
+    """Synthetic random-init experts for cfg, cached per (cfg, bits, shared, seed);
+    the least recently used store beyond _MAX_STORES is dropped (engines still
+    holding it keep it alive until they close)."""
     from .experts import ExpertStore
 
     key = (cfg.num_layers, cfg.num_experts, cfg.hidden_dim, cfg.intermediate_dim, tuple(sorted(set(bits))),
            shared_intermediate, seed)
-    if key not in _STORES:
+    if key in _STORES:
+        _STORES[key] = _STORES.pop(key)  # most recently used last
+    else:
+        while len(_STORES) >= _MAX_STORES:
+            _STORES.pop(next(iter(_STORES)))
         _STORES[key] = ExpertStore(cfg, bits=bits, seed=seed, shared_intermediate=shared_intermediate)
     return _STORES[key]
+
+
+def release_pools() -> None:
+    """Close every idle engine and drop the cached expert stores (their device
+    slot pools and pinned host pools are freed once nothing references them)."""
+    for engines in _IDLE.values():
+        for e in engines:
+            e.close()
+    _IDLE.clear()
+    _STORES.clear()
 
 
 def knobs_for(strategy: Strategy, plan: CachePlan, n: int):
@@ -173,7 +191,10 @@ _IDLE: dict = {}
 
 
 def _release(key, eng) -> None:
-    _IDLE.setdefault(key, []).append(eng)
+    pool = _IDLE.setdefault(key, [])
+    pool.append(eng)
+    while len(pool) > _MAX_IDLE:
+        pool.pop(0).close()
 
 
 def bind_engine(cache: LayeredExpertCache | None, plan: CachePlan, cfg: ModelConfig, weights, experts, knobs,
@@ -190,7 +211,9 @@ def bind_engine(cache: LayeredExpertCache | None, plan: CachePlan, cfg: ModelCon
 
     cache = cache if cache is not None else LayeredExpertCache(plan)
     if cache.engine is None:
-        key = (id(experts), tuple(plan.per_layer_capacity), id(weights))
+        # an engine's slot stride fits the widest format its first strategy needed
+        width = max(knobs.cached_bits, knobs.prefetch_bits, knobs.ondemand_bits, knobs.prefill_ondemand_bits)
+        key = (id(experts), tuple(plan.per_layer_capacity), id(weights), width)
         idle = [e for e in _IDLE.get(key, []) if e.max_tokens >= max_tokens]
         if idle:
             eng = idle[0]
@@ -210,12 +233,28 @@ def bind_engine(cache: LayeredExpertCache | None, plan: CachePlan, cfg: ModelCon
     return cache, eng
 
 
-def _check_weights(weights, cfg: ModelConfig):
+_NO_GATES: dict = {}
+
+
+def _check_weights(weights, cfg: ModelConfig, strategy: Strategy):
+    """The gate weights the engine routes with.  ``None`` is accepted where the
+    reference accepts it -- no cross-layer predictor (LoD, EAP, or fate without a
+    prefetch policy; pipeline.py:330-334, 570) -- and then stands for an all-zero
+    router: every cache decision follows the trace's chosen sets (as in the
+    reference, pipeline.py:422) and the expert outputs are combined with the
+    uniform routing weight 1/E."""
     if weights is None:
-        raise InvalidConfig("the B200 engine recomputes routing on the device from the gate inputs; "
-                            "pass the trace's GateWeights")
+        if strategy.kind == "fate" and strategy.prefetch_policy is not None:
+            raise InvalidConfig("cross-layer prediction requires gate weights")
+        key = (cfg.num_layers, cfg.num_experts, cfg.hidden_dim)
+        if key not in _NO_GATES:
+            from .gatesim import GateWeights
+            z = np.zeros((cfg.num_experts, cfg.hidden_dim))
+            _NO_GATES[key] = GateWeights(matrices=(z,) * cfg.num_layers, temperatures=(1.0,) * cfg.num_layers)
+        return _NO_GATES[key]
     if weights.num_layers != cfg.num_layers or weights.matrices[0].shape != (cfg.num_experts, cfg.hidden_dim):
         raise InvalidConfig("gate weights do not match the model geometry")
+    return weights
 
 
 def _resident_counts(logs, caps, L):
@@ -248,8 +287,12 @@ def _warn_mismatch(stats: dict) -> None:
 def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, timing: TimingModel, cfg: ModelConfig,
                       weights=None, cache: LayeredExpertCache | None = None, predictor=None,
                       collect_cache_events: bool = False, *, experts=None, shared_intermediate: int = 0,
-                      return_result: bool = False, _eap_continue: bool = False):
+                      return_result: bool = False, _eap_continue: bool = False, engine_tokens: int = 0):
     """Execute decoding of ``trace`` on the GPU (pipeline.py:343-517 semantics).
+
+    ``engine_tokens`` sizes a newly bound engine for at least that many tokens
+    (compare_strategies passes the longer of its two traces, so a decode longer
+    than the prefill that warmed the cache runs on the same engine).
 
     Strategy.eap() starts from empty co-activation statistics, as a fresh
     EapDecodePredictor does; compare_strategies passes ``_eap_continue`` so the
@@ -262,20 +305,21 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     if predictor is not None and not isinstance(predictor, CrossLayerDecodePredictor):
         raise InvalidConfig("the B200 engine fuses the cross-layer predictor into its gate kernel; "
                             "custom host predictors are not supported")
-    _check_weights(weights, cfg)
+    gates = _check_weights(weights, cfg, strategy)
     n = transfer_budget(timing, strategy.prefetch_bits())
     knobs = knobs_for(strategy, plan, n)
     if experts is None:
         experts = default_store(cfg, _bits_needed(strategy, plan), shared_intermediate)
     toks, g, ch = trace.dense_arrays(cfg)
-    cache, eng = bind_engine(cache, plan, cfg, weights, experts, knobs, max_tokens=max(len(toks), 1))
+    cache, eng = bind_engine(cache, plan, cfg, gates, experts, knobs, max_tokens=max(len(toks), engine_tokens, 1))
     if strategy.kind == "eap" and not _eap_continue:
         eng.reset_eap()
     dev = torch.device("cuda", eng.device)
     res = eng.decode(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev), tokens=toks,
                      want_logs=collect_cache_events or return_result == "logs")
     st = res.stats
-    _warn_mismatch(st)
+    if weights is not None:
+        _warn_mismatch(st)
     L = cfg.num_layers
     events = []
     stall = 0.0
@@ -316,7 +360,7 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
 
 def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timing: TimingModel, cfg: ModelConfig,
                      weights=None, cache: LayeredExpertCache | None = None, eap_stats=None, *, experts=None,
-                     shared_intermediate: int = 0, return_result: bool = False):
+                     shared_intermediate: int = 0, return_result: bool = False, engine_tokens: int = 0):
     """Execute prompt processing of ``trace`` on the GPU (pipeline.py:536-778 semantics)."""
     import torch
 
@@ -326,18 +370,19 @@ def simulate_prefill(trace: GateTrace, strategy: Strategy, plan: CachePlan, timi
     if eap_stats is not None:
         raise InvalidConfig("the B200 engine keeps EAP statistics on the device; pass eap_stats=None "
                             "(compare_strategies shares them between prefill and decode)")
-    _check_weights(weights, cfg)
+    gates = _check_weights(weights, cfg, strategy)
     n = transfer_budget(timing, strategy.prefetch_bits()) if strategy.prefetch_bits() in timing.t_expert_io else 0
     knobs = knobs_for(strategy, plan, n)
     if experts is None:
         experts = default_store(cfg, _bits_needed(strategy, plan), shared_intermediate)
     toks, g, ch = trace.dense_arrays(cfg)
-    cache, eng = bind_engine(cache, plan, cfg, weights, experts, knobs, max_tokens=max(len(toks), 1))
+    cache, eng = bind_engine(cache, plan, cfg, gates, experts, knobs, max_tokens=max(len(toks), engine_tokens, 1))
     if strategy.kind == "eap":
         eng.reset_eap()  # a fresh EapStats (pipeline.py:572-574)
     dev = torch.device("cuda", eng.device)
     Y, st, logs, step_ms, copies = eng.prefill(torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev))
-    _warn_mismatch(st)
+    if weights is not None:
+        _warn_mismatch(st)
     events = []
     stall = 0.0
     for l, row in enumerate(step_ms):
@@ -395,7 +440,9 @@ def compare_strategies(cfg: ModelConfig, timing: TimingModel, strategies: Sequen
         for s in strategies:
             plan = zero_plan(cfg, budget) if s.kind == "lod" else shared_plan
             cache = LayeredExpertCache(plan)
-            kw = dict(experts=experts, shared_intermediate=shared_intermediate)
+            kw = dict(experts=experts, shared_intermediate=shared_intermediate,
+                      engine_tokens=max(decode_trace.num_tokens,
+                                        prefill_trace.num_tokens if prefill_trace is not None else 0))
             if prefill_trace is not None:
                 tl, rep = simulate_prefill(prefill_trace, s, plan, timing, cfg, weights=weights, cache=cache, **kw)
                 rows.append(ComparisonRow(s.kind, "prefill", budget, rep, tl))
