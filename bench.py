@@ -307,9 +307,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one GPU per rank; more ranks than GPUs (functional runs on a 1-GPU box) share
+    # devices, and NCCL cannot place two ranks on one device, so those use gloo
+    ndev = torch.cuda.device_count()
+    oversub = world > ndev
+    local_dev = local % ndev
+    torch.cuda.set_device(local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversub:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_dev))
+    red_dev = torch.device("cpu") if oversub else torch.device("cuda", local_dev)
 
     from paper_2502_12224_b200 import pipeline as P
     from paper_2502_12224_b200.cache import LayeredExpertCache, plan_allocation
@@ -321,13 +330,17 @@ def main():
     cfg = qwen_cfg()
     T = args.tokens
     trace, weights = make_trace(cfg, T, seed=rank)
-    store = ExpertStore(cfg, bits=(4, 2), seed=0 if args.peer_fetch else rank, shared_intermediate=QWEN["shared"],
-                        shared_bits=16)
+    # one model, replicas serve independent request streams (trace seed = rank); the
+    # packed expert pools live once per node in /dev/shm, filled by local rank 0 and
+    # page-locked by every rank, instead of a private pinned pool each
+    shm = f"fate_bench_{os.environ.get('MASTER_PORT', '0')}" if world > 1 else None
+    store = ExpertStore(cfg, bits=(4, 2), seed=0, shared_intermediate=QWEN["shared"], shared_bits=16, shm=shm,
+                        shm_owner=local == 0, barrier=dist.barrier if world > 1 else None)
     budget = cfg.dense_bytes + QWEN["slots"] * cfg.expert_bytes[4]
     plan = plan_allocation(cfg, budget, 4)
     strategy = P.Strategy.fate()
     _, g, ch = trace.dense_arrays(cfg)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local_dev)
     gd, chd = torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev)
 
     # -- measured TimingModel -> n (transfer_budget, pipeline.py:151-156)
@@ -362,7 +375,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     stats = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         t_wall = time.perf_counter()
         for _ in range(args.steps):
             eng.reset_cache()
@@ -371,7 +384,7 @@ def main():
     torch.cuda.synchronize()
     gpu_s = sum(s["gpu_ms"] for s in stats) / 1000.0
     if world > 1:
-        t = torch.tensor([gpu_s], device=dev, dtype=torch.float64)
+        t = torch.tensor([gpu_s], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         gpu_s = float(t.item())
         dist.barrier()
@@ -456,7 +469,7 @@ def main():
             pst.append(eng.decode(gd, chd).stats)
         p_s = sum(x["gpu_ms"] for x in pst) / 1000.0
         if world > 1:
-            tt = torch.tensor([p_s], device=dev, dtype=torch.float64)
+            tt = torch.tensor([p_s], device=red_dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             p_s = float(tt.item())
         peer = {"workload": f"Qwen1.5-MoE shape decode, experts sharded over {world} GPU(s), misses served "
@@ -488,7 +501,10 @@ def main():
                        "plan": list(plan.per_layer_capacity), "tokens_per_step": T, "strategy": "fate",
                        "transfer_budget_n": n, "timing_model_ms": timing.to_dict(), "cache_start": "cold each step",
                        "l2": "inputs larger than L2 (1.95 GB slot pool + 12.5 GB pinned host pools)",
-                       "parallelism": f"replicas x{world}"},
+                       "parallelism": f"replicas x{world}",
+                       "devices": ndev if oversub else world,
+                       "host_pools": "one /dev/shm copy per node, page-locked by every rank" if world > 1
+                       else "pinned, private"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": load_traffic()[0],
                          "traffic_source": load_traffic()[1],
@@ -518,6 +534,10 @@ def main():
     if eng is not None:
         eng.close()
     if world > 1:
+        store.close()
+        dist.barrier()
+        if local == 0:
+            store.remove_shared()
         dist.destroy_process_group()
 
 

@@ -191,6 +191,13 @@ int fate_engine_set_expert_sources(fate_engine *eng, int bits, const uint8_t *co
 int fate_ipc_get_handle(const void *dev_ptr, uint8_t *handle64, int64_t *offset);
 int fate_ipc_open_handle(const uint8_t *handle64, void **dev_ptr_out);
 int fate_ipc_close(void *dev_ptr);
+/* Node-wide shared expert pools: page-lock an existing host
+ * mapping (a /dev/shm segment every rank maps) in this process, portable
+ * across devices, so transfers from it are pinned-memory DMA; and undo it.
+ * Replaces the per-process pinned pools the reference's single-process
+ * simulator never needed (it keeps no weights). */
+int fate_host_register(void *host_ptr, int64_t bytes);
+int fate_host_unregister(void *host_ptr);
 /* Shared expert for layer l: a packed device buffer (resident, dense bytes). */
 int fate_engine_set_shared(fate_engine *eng, int layer, const uint8_t *buf_dev);
 

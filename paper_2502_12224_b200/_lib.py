@@ -88,6 +88,8 @@ SIGNATURES = {
     "fate_ipc_get_handle": (c_int, [c_vp, c_vp, C.POINTER(c_i64)]),
     "fate_ipc_open_handle": (c_int, [c_vp, C.POINTER(c_vp)]),
     "fate_ipc_close": (c_int, [c_vp]),
+    "fate_host_register": (c_int, [c_vp, c_i64]),
+    "fate_host_unregister": (c_int, [c_vp]),
     "fate_ffn_decode_timed": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_int,
                                       c_vp, C.POINTER(C.c_float)]),
     "fate_k1_profile": (c_int, [c_vp]),

@@ -1095,6 +1095,20 @@ extern "C" int fate_ipc_close(void *dev_ptr) {
   return FATE_OK;
 }
 
+extern "C" int fate_host_register(void *host_ptr, int64_t bytes) {
+  if (!host_ptr || bytes <= 0) {
+    set_error("fate_host_register: bad arguments");
+    return FATE_EINVAL;
+  }
+  FATE_CUDA(cudaHostRegister(host_ptr, (size_t)bytes, cudaHostRegisterPortable));
+  return FATE_OK;
+}
+
+extern "C" int fate_host_unregister(void *host_ptr) {
+  FATE_CUDA(cudaHostUnregister(host_ptr));
+  return FATE_OK;
+}
+
 extern "C" int fate_engine_set_shared(fate_engine *g, int layer, const uint8_t *buf_dev) {
   if (layer < 0 || layer >= g->cfg.num_layers || !g->cfg.shared_intermediate) {
     set_error("fate_engine_set_shared: bad layer or engine has no shared expert");

@@ -23,6 +23,8 @@
 // of item n + 1.  Operands are bf16, accumulation fp32.
 #include <cuda_bf16.h>
 
+#include <mutex>
+
 #include "fate_internal.cuh"
 
 namespace fate {
@@ -478,24 +480,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
-int g_sms = 0;
+// per-device one-time setup (kernel attributes live in each device's context)
+struct K4Dev {
+  int sms = 0;
+  bool configured = false;
+};
+std::mutex g_k4_mu;
+K4Dev g_k4[64];
 
 }  // namespace
 
 constexpr size_t kUpSmem = (size_t)kUpStages * 3 * kTileBytes;
 constexpr size_t kDnSmem = (size_t)kDnStages * 2 * kTileBytes;
 
-cudaError_t k4_tc_preload() {
-  cudaError_t e = cudaFuncSetAttribute(k4_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpSmem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k4_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDnSmem);
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!g_sms) g_sms = 148;
+static cudaError_t k4_device(int *sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_k4_mu);
+  K4Dev &D = g_k4[dev];
+  if (!D.configured) {
+    e = cudaFuncSetAttribute(k4_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k4_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDnSmem);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&D.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    D.configured = true;
   }
-  return e;
+  *sms = D.sms;
+  return cudaSuccess;
+}
+
+cudaError_t k4_tc_preload() {
+  int sms = 0;
+  return k4_device(&sms);
 }
 
 int k4_tc_items(int n_tok, int I, int H, bool down) { return ((n_tok + BN - 1) / BN) * ((down ? H : I) / BM); }
@@ -504,11 +523,10 @@ int k4_tc_items(int n_tok, int I, int H, bool down) { return ((n_tok + BN - 1) /
 cudaError_t launch_k4_tc(const void *Xb_, int H, const PrefillExpert *ex_dev, int n, const int32_t *tok_idx,
                          const int32_t *zrow, const int *a_off_dev, void *A, float *Z, int items_up, int items_down,
                          cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = k4_tc_preload();
+  int g_sms = 0;
+  {
+    cudaError_t e = k4_device(&g_sms);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   if (n > kMaxPrefillExperts) return cudaErrorInvalidValue;
   __nv_bfloat16 *Ab = reinterpret_cast<__nv_bfloat16 *>(A);

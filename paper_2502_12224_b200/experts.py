@@ -16,6 +16,8 @@ parity tests.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import ops
@@ -27,9 +29,44 @@ def _align(x: int, a: int = 4096) -> int:
     return (x + a - 1) // a * a
 
 
+def shared_host_pool(name: str, nbytes: int, create: bool) -> torch.Tensor:
+    """A uint8 host tensor backed by the POSIX shared-memory segment
+    /dev/shm/<name> (MAP_SHARED): every process of the node that maps the same
+    name sees the same bytes, so one physical copy of the expert pools serves all
+    ranks.  ``create`` sizes the segment; the others only map it."""
+    path = os.path.join("/dev/shm", name)
+    if create:
+        with open(path, "wb") as fh:
+            fh.truncate(nbytes)
+    elif os.path.getsize(path) != nbytes:
+        raise InvalidConfig(f"shared pool {path} has {os.path.getsize(path)} bytes, expected {nbytes}")
+    return torch.from_file(path, shared=True, size=nbytes, dtype=torch.uint8)
+
+
+def register_host(t: torch.Tensor) -> None:
+    """Page-lock an existing host mapping for this process (cudaHostRegister,
+    portable), so the copy engines DMA from it like from pinned memory."""
+    from . import _lib
+    import ctypes as C
+    _lib.check(_lib.lib().fate_host_register(C.c_void_p(t.data_ptr()), C.c_int64(t.numel())), "fate_host_register")
+
+
+def unregister_host(t: torch.Tensor) -> None:
+    from . import _lib
+    import ctypes as C
+    _lib.lib().fate_host_unregister(C.c_void_p(t.data_ptr()))
+
+
 class ExpertStore:
+    """``shm``: name prefix of node-wide shared host pools (``shared_host_pool``):
+    the rank with ``shm_owner`` True creates and fills them, the others map the
+    same segments once ``barrier`` (e.g. torch.distributed.barrier) returns, and
+    every rank page-locks its mapping.  Without ``shm`` each store pins a private
+    pool."""
+
     def __init__(self, cfg: ModelConfig, bits=(4, 2), seed: int = 0, shared_intermediate: int = 0,
-                 shared_bits: int = 16, init_scale: float = 0.02, device=None, chunk: int = 32):
+                 shared_bits: int = 16, init_scale: float = 0.02, device=None, chunk: int = 32,
+                 shm: str | None = None, shm_owner: bool = True, barrier=None):
         self.cfg = cfg
         self.H, self.I = cfg.hidden_dim, cfg.intermediate_dim
         if self.I * 6 * self.H != cfg.expert_bytes[16]:
@@ -40,14 +77,34 @@ class ExpertStore:
         self.bits = tuple(sorted(set(int(b) for b in bits), reverse=True))
         self._pool: dict[int, torch.Tensor] = {}
         self._stride: dict[int, int] = {}
+        self._registered: list = []
+        self.shm = shm
         L, E = cfg.num_layers, cfg.num_experts
         for b in self.bits:
             nb = ops.expert_buffer_bytes(self.H, self.I, b)
             if b in cfg.expert_bytes and nb - 256 != cfg.expert_bytes[b]:
                 raise InvalidConfig(f"expert_bytes[{b}]={cfg.expert_bytes[b]} != packed payload {nb - 256}")
             self._stride[b] = _align(nb)
-            self._pool[b] = torch.empty((L * E, self._stride[b]), dtype=torch.uint8, pin_memory=True)
-        self._fill(chunk)
+            if shm:
+                if shm_owner:
+                    flat = shared_host_pool(f"{shm}_{b}", L * E * self._stride[b], True)
+                    register_host(flat)
+                    self._registered.append(flat)
+                    self._pool[b] = flat.view(L * E, self._stride[b])
+            else:
+                self._pool[b] = torch.empty((L * E, self._stride[b]), dtype=torch.uint8, pin_memory=True)
+        if not shm or shm_owner:
+            self._fill(chunk)
+        if shm:
+            torch.cuda.synchronize()
+            if barrier is not None:
+                barrier()  # the owner's pools are complete
+            if not shm_owner:
+                for b in self.bits:
+                    flat = shared_host_pool(f"{shm}_{b}", L * E * self._stride[b], False)
+                    register_host(flat)
+                    self._registered.append(flat)
+                    self._pool[b] = flat.view(L * E, self._stride[b])
         self._shared = []
         if self.shared_intermediate:
             for l in range(L):
@@ -107,3 +164,17 @@ class ExpertStore:
 
     def host_bytes(self) -> int:
         return sum(p.numel() for p in self._pool.values())
+
+    def close(self) -> None:
+        """Unregister shared pools (the segments stay until ``remove_shared``)."""
+        for t in self._registered:
+            unregister_host(t)
+        self._registered = []
+
+    def remove_shared(self) -> None:
+        """Delete this store's /dev/shm segments (owner, after every rank closed)."""
+        if self.shm:
+            for b in self.bits:
+                p = os.path.join("/dev/shm", f"{self.shm}_{b}")
+                if os.path.exists(p):
+                    os.remove(p)

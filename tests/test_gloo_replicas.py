@@ -83,3 +83,47 @@ def test_shard_layout_partitions_and_addresses(L, E, G):
         for e in range(E):
             r = home_rank(l, e, E, G)
             assert tab[l * E + e] == bases[r] + slot[(l, e)] * stride
+
+
+def _shm_worker(rank, world, port, name, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2502_12224_b200.experts import shared_host_pool
+    n = 1 << 20
+    if rank == 0:
+        t = shared_host_pool(name, n, True)
+        t[:] = torch.arange(n, dtype=torch.int64).remainder(251).to(torch.uint8)
+    dist.barrier()
+    if rank != 0:
+        t = shared_host_pool(name, n, False)
+    ok = bool(torch.equal(t, torch.arange(n, dtype=torch.int64).remainder(251).to(torch.uint8)))
+    dist.barrier()
+    if rank == 1:
+        t[0] = 77  # a write by one rank is seen by the other (one physical copy)
+    dist.barrier()
+    seen = int(t[0])
+    q.put((rank, ok, seen))
+    dist.barrier()
+    if rank == 0:
+        os.remove(os.path.join("/dev/shm", name))
+    dist.destroy_process_group()
+
+
+def test_shared_host_pool_one_copy_across_ranks():
+    """The node-wide expert pool: every rank maps the same /dev/shm
+    segment, so the pinned host copy exists once per node instead of once per rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    name = f"fate_gloo_shm_{port}"
+    ps = [ctx.Process(target=_shm_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert out == [(0, True, 77), (1, True, 77)]
