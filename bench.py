@@ -294,6 +294,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dense", action="store_true",
+                    help="execute the dense part (attention block + shared-expert gate) in the headline run too")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--peer-fetch", action="store_true",
                     help="also time the expert-sharded peer-fetch mode (one shared model across ranks)")
@@ -343,9 +345,20 @@ def main():
     dev = torch.device("cuda", local_dev)
     gd, chd = torch.as_tensor(g, device=dev), torch.as_tensor(ch, device=dev)
 
+    # the dense part of every step (attention block with a K/V cache over a 512-token
+    # prompt + Qwen's shared-expert gate) executes on the device
+    # The headline line is the MoE-layer path (the reference charges attention as the
+    # constant t_attn); --dense executes the dense part in the headline too, and the
+    # line always carries a "dense_part" measurement with it executed.
+    from paper_2502_12224_b200.dense import DenseConfig, DenseWeights
+    dense_w = DenseWeights(cfg, DenseConfig.qwen_moe(), seed=0)
+    dense = dense_w if args.dense else None
+    CTX0 = 512
     # -- measured TimingModel -> n (transfer_budget, pipeline.py:151-156)
     eng = OffloadEngine(cfg, plan.per_layer_capacity, store, weights, P.knobs_for(strategy, plan, 0),
                         max_tokens=max(T, 64))
+    if dense is not None:
+        eng.set_dense(dense, max_ctx=CTX0 + max(T, 64), ctx0=CTX0)
     cal = eng.decode(gd[:32], chd[:32])
     io = {}
     for b in (4, 2):
@@ -361,7 +374,8 @@ def main():
             e1.record(s)
         torch.cuda.synchronize()
         io[b] = e0.elapsed_time(e1) / 16
-    timing = P.TimingModel(t_moe=cal.stats["ffn_ms"] / cal.stats["steps"], t_attn=0.01,
+    t_attn = cal.stats["dense_ms"] / cal.stats["steps"] if dense is not None else 0.01
+    timing = P.TimingModel(t_moe=cal.stats["ffn_ms"] / cal.stats["steps"], t_attn=t_attn,
                            t_gate=cal.stats["gate_ms"] / cal.stats["steps"], t_expert_io={4: io[4], 2: io[2]},
                            dequant_ms=0.0)
     n = P.transfer_budget(timing, strategy.prefetch_bits())
@@ -391,7 +405,8 @@ def main():
     value = T * args.steps * world / gpu_s
     agg = {k: sum(s[k] for s in stats) for k in ("ffn_ms", "gate_ms", "ffn_bytes", "accesses", "cache_hits",
                                                    "arrival_hits", "h2d_bytes", "copy_busy_ms", "transfers_done",
-                                                   "trace_mismatches", "steps", "ondemand_issued", "prefetch_issued")}
+                                                   "trace_mismatches", "steps", "ondemand_issued", "prefetch_issued",
+                                                   "dense_ms")}
     k3_launches = agg["steps"]
     k3_ms = agg["ffn_ms"] / k3_launches
     k3_bytes = agg["ffn_bytes"] / k3_launches
@@ -418,7 +433,8 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tl, rep, res = P.simulate_decoding(trace, strategy, plan, timing, cfg, weights=weights,
-                                           cache=LayeredExpertCache(plan), experts=store, return_result=True)
+                                           cache=LayeredExpertCache(plan), experts=store, return_result=True,
+                                           dense=dense, dense_ctx0=CTX0)
         y_last = res.y[:, -1].cpu()
         torch.cuda.synchronize()
         if i:
@@ -479,6 +495,34 @@ def main():
                 "k3_ms_per_launch": sum(x["ffn_ms"] for x in pst) / sum(x["steps"] for x in pst)}
         shards.detach(eng)
         shards.close()
+    # -- the dense part executed: attention block with a K/V cache
+    # over a 512-token prompt + Qwen's shared-expert gate in every step; t_attn is then
+    # measured instead of assumed, which sets the transfer budget n of this run
+    dense_part = None
+    if dense is None:
+        eng.set_dense(dense_w, max_ctx=CTX0 + max(T, 64), ctx0=CTX0)
+        eng.set_strategy(P.knobs_for(strategy, plan, n))
+        eng.reset_cache()
+        cal_d = eng.decode(gd[:32], chd[:32]).stats
+        t_attn_d = cal_d["dense_ms"] / cal_d["steps"]
+        timing_d = P.TimingModel(t_moe=timing.t_moe, t_attn=t_attn_d, t_gate=timing.t_gate,
+                                 t_expert_io=dict(timing.t_expert_io), dequant_ms=0.0)
+        n_d = P.transfer_budget(timing_d, strategy.prefetch_bits())
+        eng.set_strategy(P.knobs_for(strategy, plan, n_d))
+        dst = []
+        for _ in range(2):
+            eng.reset_cache()
+            dst.append(eng.decode(gd, chd).stats)
+        d_s = sum(x["gpu_ms"] for x in dst) / 1000.0
+        if world > 1:
+            tt = torch.tensor([d_s], device=red_dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            d_s = float(tt.item())
+        dense_part = {"tokens_per_s": T * len(dst) * world / d_s, "dense_ms_per_step":
+                      sum(x["dense_ms"] for x in dst) / sum(x["steps"] for x in dst),
+                      "t_attn_ms_measured": t_attn_d, "transfer_budget_n": n_d,
+                      "what": f"attention (16 x 128 heads, q/k/v bias, RoPE, K/V cache over a {CTX0}-token prompt) + "
+                              "shared-expert gate executed before every gate kernel; n from the measured t_attn"}
     pre = None
     # prefill (configs[2]) is a single-GPU workload; under torchrun every rank would
     # pin its own 15 GB DeepSeek host pools, so it is measured at N = 1 only
@@ -500,6 +544,9 @@ def main():
                        "shared_intermediate": QWEN["shared"], "shared_bits": 16, "slots_int4": QWEN["slots"],
                        "plan": list(plan.per_layer_capacity), "tokens_per_step": T, "strategy": "fate",
                        "transfer_budget_n": n, "timing_model_ms": timing.to_dict(), "cache_start": "cold each step",
+                       "dense_part": "not executed in the headline (reference: constant t_attn); see dense_part"
+                       if dense is None else
+                       f"executed: attention (16 x 128 heads, K/V cache, prompt {CTX0} tokens) + shared-expert gate",
                        "l2": "inputs larger than L2 (1.95 GB slot pool + 12.5 GB pinned host pools)",
                        "parallelism": f"replicas x{world}",
                        "devices": ndev if oversub else world,
@@ -518,16 +565,21 @@ def main():
             if e2e else None,
             # per decode step K1 + the deferred ARC update + K3; per run run_begin + the final ARC flush
             # (agg["steps"] already sums the steps of all timed runs)
-            "gpu_launches": int(3 * agg["steps"] + 2 * args.steps),
+            # + with the dense part, per step QKV GEMV, RoPE/append, attention, combine, Wo
+            # GEMV, shared gate, and one embedding per token
+            "gpu_launches": int(3 * agg["steps"] + 2 * args.steps
+                                + (6 * agg["steps"] + agg["steps"] // cfg.num_layers if dense is not None else 0)),
             "clocks": clocks,
             "hit_rate_cache": agg["cache_hits"] / agg["accesses"],
             "hit_rate_combined": (agg["cache_hits"] + agg["arrival_hits"]) / agg["accesses"],
             "h2d": {"gbs": h2d_gbs, "bytes": agg["h2d_bytes"], "copies": agg["transfers_done"],
                     "ondemand": agg["ondemand_issued"], "prefetch": agg["prefetch_issued"]},
             "k1_ms_per_launch": agg["gate_ms"] / agg["steps"],
+            "dense_ms_per_step": agg["dense_ms"] / agg["steps"] if dense is not None else None,
             "trace_mismatches": agg["trace_mismatches"],
             "prefill": pre,
             "peer_fetch": peer,
+            "dense_part": dense_part,
             "wall_s_timed": wall,
         }
         print(json.dumps(out), flush=True)

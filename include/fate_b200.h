@@ -197,7 +197,30 @@ int fate_ipc_close(void *dev_ptr);
  * Replaces the per-process pinned pools the reference's single-process
  * simulator never needed (it keeps no weights). */
 int fate_host_register(void *host_ptr, int64_t bytes);
+/* Dense part of one decode step (replaces the t_attn / t_gate
+ * constants, reference core.py:79-83, pipeline.py:418, 484): h = h_prev + y_prev,
+ * qkv = Wqkv RMSNorm(h) + b, RoPE at pos, K/V appended to the bf16 cache
+ * kv[pos] ([ctx][2][nkv*hd]), o = decode attention over positions 0..pos (GQA),
+ * a = h + Wo o, and the shared-expert gate sigmoid(gate_w . sqrt(H) gate_in) into
+ * *gate_out when gate_w is given.  Device pointers; bf16 weights; synchronous.
+ * The engine runs the same kernels inside its step loop (fate_engine_set_dense). */
+int fate_dense_step(int H, int n_heads, int n_kv_heads, int head_dim, float eps, float rope_theta, const void *wqkv,
+                    const float *bqkv, const float *norm, const void *wo, void *kv, const float *gate_w,
+                    float *gate_out, const float *h_prev, const float *y_prev, const double *gate_in, int pos, float *h,
+                    float *qkv, float *q, float *o, float *a, float *part_o, float *part_ml, void *stream);
 int fate_host_unregister(void *host_ptr);
+/* The dense part of every decode step (replacing the t_attn /
+ * t_gate constants of core.py:79-83): attention geometry, K/V cache capacity
+ * max_ctx positions per layer with the prompt's ctx0 positions pre-filled
+ * (synthetic), RMSNorm eps and RoPE theta; then per layer the device weights
+ * (bf16 Wqkv [(nh+2nkv)hd, H], optional fp32 bias, fp32 RMSNorm weight, bf16 Wo
+ * [H, nh hd], optional fp32 shared-expert gate [H]; caller-owned).  Decode token
+ * t then runs at position ctx0 + t; with every layer gated, the shared expert's
+ * routing weight is sigmoid(gate . x) instead of 1. */
+int fate_engine_set_dense(fate_engine *eng, int n_heads, int n_kv_heads, int head_dim, int max_ctx, int ctx0,
+                          float eps, float rope_theta);
+int fate_engine_set_dense_layer(fate_engine *eng, int layer, const void *wqkv, const float *bqkv, const float *norm,
+                                const void *wo, const float *shared_gate_w);
 /* Shared expert for layer l: a packed device buffer (resident, dense bytes). */
 int fate_engine_set_shared(fate_engine *eng, int layer, const uint8_t *buf_dev);
 
@@ -249,6 +272,8 @@ typedef struct fate_run_stats {
   int64_t d2d_bytes;          /* misses served from device memory (local or
                                  peer HBM over NVLink, expert-sharded mode)    */
   int32_t error; int32_t pad;
+  double dense_ms;            /* summed dense-part time (attention block +
+                                 shared-expert gate, fate_engine_set_dense)    */
 } fate_run_stats;
 
 /* Decode T tokens (simulate_decoding, pipeline.py:343-517).

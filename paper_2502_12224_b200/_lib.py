@@ -63,7 +63,7 @@ class RunStats(C.Structure):
         ("transfers_done", c_i64), ("transfers_dropped", c_i64), ("h2d_bytes", c_i64),
         ("copy_busy_ms", c_dbl), ("recall_sum", c_dbl), ("recall_n", c_i64), ("trace_mismatches", c_i64),
         ("ffn_bytes", c_i64), ("ffn_flops", c_dbl), ("near_ties", c_i64), ("d2d_bytes", c_i64),
-        ("error", C.c_int32), ("pad", C.c_int32),
+        ("error", C.c_int32), ("pad", C.c_int32), ("dense_ms", c_dbl),
     ]
 
     def as_dict(self) -> dict:
@@ -89,7 +89,11 @@ SIGNATURES = {
     "fate_ipc_open_handle": (c_int, [c_vp, C.POINTER(c_vp)]),
     "fate_ipc_close": (c_int, [c_vp]),
     "fate_host_register": (c_int, [c_vp, c_i64]),
+    "fate_dense_step": (c_int, [c_int, c_int, c_int, c_int, C.c_float, C.c_float] + [c_vp] * 10 + [c_int]
+                        + [c_vp] * 8),
     "fate_host_unregister": (c_int, [c_vp]),
+    "fate_engine_set_dense": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, C.c_float, C.c_float]),
+    "fate_engine_set_dense_layer": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fate_ffn_decode_timed": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_int,
                                       c_vp, C.POINTER(C.c_float)]),
     "fate_k1_profile": (c_int, [c_vp]),

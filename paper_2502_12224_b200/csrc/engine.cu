@@ -544,7 +544,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (lane == 0) {
     int n = k, off = k * d.I;
     if (S.shared_present) {
-      B.e[n] = FfnExpert{d.shared[layer], 1.0f, d.I_shared, d.shared_bits, off, 0};
+      B.e[n] = FfnExpert{d.shared[layer], d.shared_gate ? d.shared_gate[layer] : 1.0f, d.I_shared, d.shared_bits, off,
+                         0};
       off += d.I_shared;
       ++n;
     }
@@ -763,6 +764,14 @@ struct fate_engine {
   void *pf_block = nullptr;
   std::mutex mu;
   // last run's timeline (ms from the run's first event)
+  // dense part (attention block + shared-expert gate), enabled by fate_engine_set_dense
+  bool dense = false;
+  DenseDims dd{};
+  int max_ctx = 0, ctx0 = 0;
+  std::vector<DenseLayer> dl;
+  void *dense_block = nullptr;  // K/V cache + scratch + shared-gate outputs
+  DenseScratch ds{};
+  float *shared_gate_dev = nullptr;
   std::vector<double> step_ms;     // [steps][4]: gate start/end, moe start/end
   std::vector<double> copy_ms;     // [copies][2]
   std::vector<int32_t> copy_meta;  // [copies][5]: kind, step, layer, expert, bits
@@ -1002,6 +1011,7 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   cudaFree(g->dev_block);
   if (g->k3_scratch) cudaFree(g->k3_scratch);
   if (g->pf_block) cudaFree(g->pf_block);
+  if (g->dense_block) cudaFree(g->dense_block);
   cudaFreeHost(g->ring_host);
   cudaFreeHost((void *)g->ready_host);
   delete g;
@@ -1106,6 +1116,82 @@ extern "C" int fate_host_register(void *host_ptr, int64_t bytes) {
 
 extern "C" int fate_host_unregister(void *host_ptr) {
   FATE_CUDA(cudaHostUnregister(host_ptr));
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_dense(fate_engine *g, int n_heads, int n_kv_heads, int head_dim, int max_ctx, int ctx0,
+                                     float eps, float rope_theta) {
+  const int H = g->cfg.hidden_dim, L = g->cfg.num_layers;
+  if (H % 256 || head_dim % 32 || head_dim > 128 || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads ||
+      n_heads / n_kv_heads > 32 || max_ctx < 1 || ctx0 < 0 || ctx0 >= max_ctx || max_ctx > 32 * kDenseMaxSplits) {
+    set_error("fate_engine_set_dense: unsupported geometry (head_dim <= 128, max_ctx <= 4096)");
+    return FATE_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(g->mu);
+  cudaSetDevice(g->cfg.device);
+  if (g->dense_block && g->dd.n_heads == n_heads && g->dd.n_kv_heads == n_kv_heads && g->dd.head_dim == head_dim &&
+      g->max_ctx >= max_ctx && g->ctx0 == ctx0) {
+    g->dd.eps = eps, g->dd.rope_theta = rope_theta;  // same cache: the prompt positions are kept
+    return FATE_OK;
+  }
+  if (g->dense_block) {
+    cudaStreamSynchronize(g->cstream);
+    cudaFree(g->dense_block);
+    g->dense_block = nullptr;
+  }
+  const int64_t row = (int64_t)2 * n_kv_heads * head_dim, nq = (int64_t)(n_heads + 2 * n_kv_heads) * head_dim;
+  const int64_t kv_elems = (int64_t)L * max_ctx * row;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t o_kv = carve(kv_elems * 2), o_h = carve(H * 4), o_qkv = carve(nq * 4), o_q = carve(n_heads * head_dim * 4),
+               o_o = carve(n_heads * head_dim * 4), o_a = carve(H * 4),
+               o_po = carve((size_t)kDenseMaxSplits * n_heads * head_dim * 4),
+               o_ml = carve((size_t)kDenseMaxSplits * n_heads * 8), o_sg = carve((size_t)L * 4),
+               o_cnt = carve((size_t)n_heads * 4);
+  FATE_CUDA(cudaMalloc(&g->dense_block, off));
+  uint8_t *b = (uint8_t *)g->dense_block;
+  g->ds = DenseScratch{(float *)(b + o_h), (float *)(b + o_qkv), (float *)(b + o_q), (float *)(b + o_o),
+                       (float *)(b + o_po), (float *)(b + o_a), (float2 *)(b + o_ml), (unsigned *)(b + o_cnt)};
+  FATE_CUDA(cudaMemsetAsync(b + o_cnt, 0, (size_t)n_heads * 4, g->cstream));
+  g->shared_gate_dev = (float *)(b + o_sg);
+  // the prompt's K/V (positions < ctx0 of every layer): synthetic, deterministic
+  FATE_CUDA(launch_fill_kv((__nv_bfloat16 *)(b + o_kv), kv_elems, 0x9e3779b9u, g->cstream));
+  FATE_CUDA(cudaStreamSynchronize(g->cstream));
+  g->dd = DenseDims{H, n_heads, n_kv_heads, head_dim, eps, rope_theta, kDenseMaxSplits};
+  g->max_ctx = max_ctx;
+  g->ctx0 = ctx0;
+  g->dl.assign(L, DenseLayer{});
+  for (int l = 0; l < L; ++l) {
+    g->dl[l].kv = (__nv_bfloat16 *)(b + o_kv) + (int64_t)l * max_ctx * row;
+    g->dl[l].shared_gate_out = g->shared_gate_dev + l;
+  }
+  g->dense = false;  // until every layer has its weights
+  return FATE_OK;
+}
+
+extern "C" int fate_engine_set_dense_layer(fate_engine *g, int layer, const void *wqkv, const float *bqkv,
+                                           const float *norm, const void *wo, const float *shared_gate_w) {
+  if (!g->dense_block || layer < 0 || layer >= g->cfg.num_layers || !wqkv || !norm || !wo) {
+    set_error("fate_engine_set_dense_layer: call fate_engine_set_dense first; wqkv, norm and wo are required");
+    return FATE_EINVAL;
+  }
+  DenseLayer &D = g->dl[layer];
+  D.wqkv = (const __nv_bfloat16 *)wqkv;
+  D.bqkv = bqkv;
+  D.norm = norm;
+  D.wo = (const __nv_bfloat16 *)wo;
+  D.shared_gate = shared_gate_w;
+  bool all = true, gated = false;
+  for (const DenseLayer &x : g->dl) all = all && x.wqkv, gated = gated || x.shared_gate;
+  g->dense = all;
+  // K1 reads the gate only when every layer is gated (else the shared weight stays 1)
+  bool every = all;
+  for (const DenseLayer &x : g->dl) every = every && x.shared_gate;
+  g->d.shared_gate = all && every && gated ? g->shared_gate_dev : nullptr;
   return FATE_OK;
 }
 
@@ -1366,13 +1452,22 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   if (serial_launches())
     if (int st = ch.init_serial()) return st;
   std::vector<cudaEvent_t> kev;  // per step: K1 start, K1 end, K3 start (after the wait), K3 end
+  std::vector<cudaEvent_t> dev_;  // per step with the dense part: its start, end
+  if (g->dense && g->ctx0 + T > g->max_ctx) {
+    set_error("fate_engine_decode: prompt context + tokens exceed the dense part's max_ctx");
+    return FATE_EINVAL;
+  }
   if (timed) {
     ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
     for (auto &e : ch.ev) FATE_CUDA(cudaEventCreate(&e));
     for (int i = (int)ch.ev.size() - 2; i >= 0; i -= 2) ch.ev_free.push_back(i);
     kev.resize(4 * (size_t)n_steps);
     for (auto &e : kev) FATE_CUDA(cudaEventCreate(&e));
-    ch.t0 = kev[0];
+    if (g->dense) {
+      dev_.resize(2 * (size_t)n_steps);
+      for (auto &e : dev_) FATE_CUDA(cudaEventCreate(&e));
+    }
+    ch.t0 = g->dense ? dev_[0] : kev[0];
   }
   g->step_ms.clear();
   g->copy_ms.clear();
@@ -1440,6 +1535,15 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       // tail block + router rows of W_l (and W_{l+1} when predicting)
       const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
       FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));  // previous step's ARC update applied
+      if (g->dense) {
+        // the dense part of (t, l): attention block + shared-expert gate (dense.cu)
+        if (timed) FATE_CUDA(cudaEventRecord(dev_[2 * s], cs));
+        const double *gi = gate_in_dev + ((int64_t)t * L + l) * H;
+        if (l == 0) FATE_CUDA(launch_embed(gi, H, g->ds.a, cs));
+        FATE_CUDA(launch_dense_step(g->dl[l], g->dd, g->ds.a, l == 0 ? nullptr : y_dev + ((int64_t)t * L + l - 1) * H,
+                                    gi, g->ctx0 + t, g->ds, cs));
+        if (timed) FATE_CUDA(cudaEventRecord(dev_[2 * s + 1], cs));
+      }
       if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
       decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
                                                         (volatile uint32_t *)g->ready_dev, t);
@@ -1573,24 +1677,32 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   }
   if (timed && status == FATE_OK) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, kev[0], kev[4 * (n_steps - 1) + 3]);
+    const cudaEvent_t t0 = ch.t0;
+    cudaEventElapsedTime(&ms, t0, kev[4 * (n_steps - 1) + 3]);
     st.gpu_ms = ms;
-    double ffn = 0.0, gate = 0.0;
+    double ffn = 0.0, gate = 0.0, dense = 0.0;
     g->step_ms.resize(4 * (size_t)n_steps);
     for (int s = 0; s < n_steps; ++s) {
       float t[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int j = 1; j < 4; ++j) cudaEventElapsedTime(&t[j], kev[0], kev[4 * s + j]);
-      if (s) cudaEventElapsedTime(&t[0], kev[0], kev[4 * s]);
+      for (int j = 0; j < 4; ++j)
+        if (s || j || g->dense) cudaEventElapsedTime(&t[j], t0, kev[4 * s + j]);
       for (int j = 0; j < 4; ++j) g->step_ms[4 * (size_t)s + j] = t[j];
       gate += t[1] - t[0];
       ffn += t[3] - t[2];
+      if (g->dense) {
+        float d = 0.f;
+        cudaEventElapsedTime(&d, dev_[2 * s], dev_[2 * s + 1]);
+        dense += d;
+      }
     }
     st.ffn_ms = ffn;
     st.gate_ms = gate;
+    st.dense_ms = dense;
   }
   if (timed) {
     for (auto &e : ch.ev) cudaEventDestroy(e);
     for (auto &e : kev) cudaEventDestroy(e);
+    for (auto &e : dev_) cudaEventDestroy(e);
   }
   st.steps = n_steps;
   st.accesses = (int64_t)ds.accesses;

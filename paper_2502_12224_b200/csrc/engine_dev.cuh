@@ -71,6 +71,7 @@ struct EngineDev {
   int64_t buf_stride;
   uint8_t *pool;              // nbuf * buf_stride
   const uint8_t **shared;     // [L] shared-expert buffers (or null)
+  const float *shared_gate;   // [L] sigmoid gate of the shared expert (dense part), or null: weight 1
   const double *W;            // [L, E, H]
   const double *tau;          // [L]
   ArcLayer *arc;              // [L]

@@ -173,6 +173,32 @@ __device__ inline void write_xlay(const float *x, int H, float4 *xlay, int tid, 
 
 cudaError_t ffn_preload();
 
+// Dense part of a decode step (dense.cu): attention block + shared-expert gate.
+struct DenseDims {
+  int H, n_heads, n_kv_heads, head_dim;
+  float eps, rope_theta;
+  int max_splits;
+};
+struct DenseLayer {
+  const __nv_bfloat16 *wqkv;  // [(nh + 2 nkv) hd, H] row-major
+  const float *bqkv;          // [(nh + 2 nkv) hd] or null
+  const float *norm;          // RMSNorm weight [H]
+  const __nv_bfloat16 *wo;    // [H, nh hd]
+  __nv_bfloat16 *kv;          // K/V cache [max_ctx][2][nkv hd]
+  const float *shared_gate;   // [H] or null (no gated shared expert)
+  float *shared_gate_out;     // sigmoid(w . x) of the step
+};
+struct DenseScratch {
+  float *h, *qkv, *q, *o, *part_o, *a;
+  float2 *part_ml;
+  unsigned *cnt;  // [n_heads] split-completion counters (zero between steps)
+};
+constexpr int kDenseMaxSplits = 128;  // context positions <= 32 * kDenseMaxSplits
+cudaError_t launch_dense_step(const DenseLayer &Ly, const DenseDims &D, const float *h_prev, const float *y_prev,
+                              const double *gate_in, int pos, DenseScratch &S, cudaStream_t s);
+cudaError_t launch_embed(const double *gate_in, int H, float *h, cudaStream_t s);
+cudaError_t launch_fill_kv(__nv_bfloat16 *kv, int64_t n, uint32_t seed, cudaStream_t s);
+
 // K1 kernels exposed to the engine.
 cudaError_t launch_gate_batch(const double *W, double tau, const double *h, int64_t h_stride, int T, int E, int H,
                               double *routing, int32_t *order, int32_t *list_len, int top_k, int policy,

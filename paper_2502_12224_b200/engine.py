@@ -89,6 +89,22 @@ class OffloadEngine:
             p_int2=k.p_int2, prefill_ondemand_bits=k.prefill_ondemand_bits, max_tokens=self.max_tokens,
             max_inflight=k.max_inflight, device=self.device)
 
+    def set_dense(self, dense, max_ctx: int, ctx0: int) -> None:
+        """Execute the dense part (``dense.DenseWeights``) in every decode step:
+        the K/V cache holds ``max_ctx`` positions per layer, the first ``ctx0`` of
+        them a synthetic prompt; decode token t runs at position ctx0 + t."""
+        dc = dense.dc
+        check(self._L.fate_engine_set_dense(self._h, dc.n_heads, dc.n_kv_heads, dc.head_dim, int(max_ctx), int(ctx0),
+                                            dc.eps, dc.rope_theta), "fate_engine_set_dense")
+        if getattr(self, "dense", None) is dense and getattr(self, "_dense_ctx", None) == (max_ctx, ctx0):
+            return
+        self._dense_ctx = (max_ctx, ctx0)
+        for l, ly in enumerate(dense.layers):
+            check(self._L.fate_engine_set_dense_layer(self._h, l, ptr(ly["wqkv"]), ptr(ly["bqkv"]), ptr(ly["norm"]),
+                                                      ptr(ly["wo"]), ptr(ly["shared_gate"])),
+                  "fate_engine_set_dense_layer")
+        self.dense = dense  # the engine reads these buffers on every step
+
     def set_strategy(self, knobs: StrategyKnobs) -> None:
         c = self._config(knobs)
         check(self._L.fate_engine_set_strategy(self._h, C.byref(c)), "fate_engine_set_strategy")

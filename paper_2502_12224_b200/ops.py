@@ -150,3 +150,21 @@ def ffn_prefill(X: torch.Tensor, bufs: list, tok_lists: list, tok_weights: list)
     check(L.fate_ffn_prefill(ptr(X.contiguous()), T, H, n, arr, ptr(idx), ptr(tw), offc, ptr(Y), _stream()),
           "fate_ffn_prefill")
     return Y
+
+
+def dense_step(dims: dict, layer: dict, kv: torch.Tensor, h_prev: torch.Tensor, y_prev, gate_in, pos: int) -> dict:
+    """One dense step (attention block + shared-expert gate) on the device,
+    ``fate_dense_step``; returns the intermediate vectors (for numerics tests)."""
+    L = _lib.lib()
+    H, nh, nkv, hd = dims["H"], dims["n_heads"], dims["n_kv_heads"], dims["head_dim"]
+    dev = h_prev.device
+    out = {k: torch.empty(n, dtype=torch.float32, device=dev) for k, n in
+           (("h", H), ("qkv", (nh + 2 * nkv) * hd), ("q", nh * hd), ("o", nh * hd), ("a", H),
+            ("part_o", 128 * nh * hd), ("part_ml", 128 * nh * 2), ("gate", 1))}
+    gw = layer.get("shared_gate")
+    check(L.fate_dense_step(H, nh, nkv, hd, dims.get("eps", 1e-6), dims.get("rope_theta", 1e6), ptr(layer["wqkv"]),
+                            ptr(layer.get("bqkv")), ptr(layer["norm"]), ptr(layer["wo"]), ptr(kv), ptr(gw),
+                            ptr(out["gate"]) if gw is not None else None, ptr(h_prev), ptr(y_prev), ptr(gate_in), pos,
+                            ptr(out["h"]), ptr(out["qkv"]), ptr(out["q"]), ptr(out["o"]), ptr(out["a"]),
+                            ptr(out["part_o"]), ptr(out["part_ml"]), _stream()), "fate_dense_step")
+    return out

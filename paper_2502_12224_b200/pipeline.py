@@ -287,12 +287,15 @@ def _warn_mismatch(stats: dict) -> None:
 def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, timing: TimingModel, cfg: ModelConfig,
                       weights=None, cache: LayeredExpertCache | None = None, predictor=None,
                       collect_cache_events: bool = False, *, experts=None, shared_intermediate: int = 0,
-                      return_result: bool = False, _eap_continue: bool = False, engine_tokens: int = 0):
+                      return_result: bool = False, _eap_continue: bool = False, engine_tokens: int = 0,
+                      dense=None, dense_ctx0: int = 0):
     """Execute decoding of ``trace`` on the GPU (pipeline.py:343-517 semantics).
 
     ``engine_tokens`` sizes a newly bound engine for at least that many tokens
     (compare_strategies passes the longer of its two traces, so a decode longer
-    than the prefill that warmed the cache runs on the same engine).
+    than the prefill that warmed the cache runs on the same engine).  ``dense``
+    (``dense.DenseWeights``) executes the attention block and shared-expert gate in
+    every step, token t at context position ``dense_ctx0`` + t.
 
     Strategy.eap() starts from empty co-activation statistics, as a fresh
     EapDecodePredictor does; compare_strategies passes ``_eap_continue`` so the
@@ -312,6 +315,8 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
         experts = default_store(cfg, _bits_needed(strategy, plan), shared_intermediate)
     toks, g, ch = trace.dense_arrays(cfg)
     cache, eng = bind_engine(cache, plan, cfg, gates, experts, knobs, max_tokens=max(len(toks), engine_tokens, 1))
+    if dense is not None:
+        eng.set_dense(dense, max_ctx=dense_ctx0 + max(len(toks), engine_tokens, 1), ctx0=dense_ctx0)
     if strategy.kind == "eap" and not _eap_continue:
         eng.reset_eap()
     dev = torch.device("cuda", eng.device)
@@ -454,12 +459,15 @@ def compare_strategies(cfg: ModelConfig, timing: TimingModel, strategies: Sequen
 
 def measure_timing_model(engine_result_stats: dict, cfg: ModelConfig, steps: int, copies, t_attn_ms: float = 0.01):
     """A TimingModel measured on this GPU: t_gate/t_moe from the per-step CUDA events,
-    t_expert_io from the copy events per bit width, dequant fused (0).  Attention is not
-    executed in this tier, so t_attn is the caller's estimate."""
+    t_expert_io from the copy events per bit width, dequant fused (0), and t_attn from
+    the dense part's events when the engine executed it (``OffloadEngine.set_dense``),
+    else the caller's estimate."""
     io = {}
     for (c0, c1, kind, step, layer, expert, bits) in copies:
         if kind in (0, 1):
             io.setdefault(bits, []).append(c1 - c0)
     t_io = {b: float(np.median(v)) for b, v in io.items()}
+    if engine_result_stats.get("dense_ms", 0.0) > 0:
+        t_attn_ms = engine_result_stats["dense_ms"] / steps
     return TimingModel(t_moe=engine_result_stats["ffn_ms"] / steps, t_attn=t_attn_ms,
                        t_gate=engine_result_stats["gate_ms"] / steps, t_expert_io=t_io, dequant_ms=0.0)
