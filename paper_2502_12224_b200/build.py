@@ -21,6 +21,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-re
 # the shipped library carries no instrumentation)
 if os.environ.get("FATE_PROF"):
     FLAGS = FLAGS + ["-DFATE_PROF"]
+# extra -D definitions for tuning experiments (profiling builds only)
+FLAGS = FLAGS + [f"-D{d}" for d in os.environ.get("FATE_DEFS", "").split() if d]
 
 
 def sources() -> list[str]:

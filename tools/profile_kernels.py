@@ -111,6 +111,11 @@ def k3prof(iters: int):
         for i, nm in enumerate(names):
             v = (P[:, i] - t0) / 1e3
             print(f"  {nm:9s} median {np.median(v):7.2f}  min {v.min():7.2f}  max {v.max():7.2f}  argmax {int(v.argmax())}")
+        nq = sum(i // 64 for i, b in spec if b != 16)
+        dr = (P[:, 3] - t0) / 1e3
+        if 0 < nq < 148:
+            print(f"  drained: CTAs with a quantized unit (< {nq}) median {np.median(dr[:nq]):.2f} max {dr[:nq].max():.2f}"
+                  f" | bf16 only median {np.median(dr[nq:]):.2f} max {dr[nq:].max():.2f}")
         S = buf[192 * 8:].reshape(256, 4).astype(np.int64)
         n = int((S[:, 1] > 0).sum())
         print("  CTA0 stages: [wait-start, full, released] us, tag (kind*1e6 + j*1e4 + rows)")
