@@ -197,6 +197,34 @@ int fate_ipc_close(void *dev_ptr);
  * Replaces the per-process pinned pools the reference's single-process
  * simulator never needed (it keeps no weights). */
 int fate_host_register(void *host_ptr, int64_t bytes);
+/* Transfer channel C1 as a standalone object (SURVEY §8b prefetch_{enqueue,
+ * promote,drop_stale,wait}): the reference's _Channel (pipeline.py:163-264) over
+ * real copies.  Pending transfers are a host FIFO; pump / wait start them in
+ * queue order as cudaMemcpyAsync on the channel's copy stream (<= max_inflight
+ * in flight for pump), each followed by an event.  device < 0: queue
+ * bookkeeping only, no CUDA calls.  The decode / prefill engine runs the same
+ * discipline internally. */
+typedef struct fate_channel fate_channel;
+int fate_channel_create(int device, int max_inflight, fate_channel **out);
+int fate_channel_destroy(fate_channel *ch);
+/* _Channel.enqueue (pipeline.py:196): kind 0 prefetch / 1 on-demand for step
+ * (token, layer), a copy of `bytes` from src (pinned host or device) to dst. */
+int fate_channel_enqueue(fate_channel *ch, int kind, int token, int layer, int expert, int bits, const void *src,
+                         void *dst, int64_t bytes, int64_t *id_out);
+/* _Channel.promote_ondemand (pipeline.py:241): on-demand ahead of prefetch, stably. */
+int fate_channel_promote(fate_channel *ch);
+/* _Channel.drop_stale (pipeline.py:247): discard pending prefetches with step <= (token, layer). */
+int fate_channel_drop_stale(fate_channel *ch, int token, int layer, int *n_dropped);
+/* _Channel.settle (pipeline.py:214): retire finished copies, start pending ones while < max_inflight. */
+int fate_channel_pump(fate_channel *ch);
+/* _Channel.completion (pipeline.py:222) for a consumer stream: start everything up to
+ * transfer `id` in queue order, then cudaStreamWaitEvent(stream, its event). */
+int fate_channel_wait(fate_channel *ch, int64_t id, void *stream);
+/* _Channel.find (pipeline.py:232): state -1 none, 0 pending, 1 in flight, 2 complete. */
+int fate_channel_find(fate_channel *ch, int token, int layer, int expert, int *state, int64_t *id_out);
+/* The pending queue in order (ids) and the number of copies in flight. */
+int fate_channel_pending(fate_channel *ch, int64_t *ids, int max, int *n, int *n_inflight);
+
 /* Dense part of one decode step (replaces the t_attn / t_gate
  * constants, reference core.py:79-83, pipeline.py:418, 484): h = h_prev + y_prev,
  * qkv = Wqkv RMSNorm(h) + b, RoPE at pos, K/V appended to the bf16 cache

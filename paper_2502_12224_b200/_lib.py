@@ -92,6 +92,15 @@ SIGNATURES = {
     "fate_dense_step": (c_int, [c_int, c_int, c_int, c_int, C.c_float, C.c_float] + [c_vp] * 10 + [c_int]
                         + [c_vp] * 8),
     "fate_host_unregister": (c_int, [c_vp]),
+    "fate_channel_create": (c_int, [c_int, c_int, C.POINTER(c_vp)]),
+    "fate_channel_destroy": (c_int, [c_vp]),
+    "fate_channel_enqueue": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_i64, C.POINTER(c_i64)]),
+    "fate_channel_promote": (c_int, [c_vp]),
+    "fate_channel_drop_stale": (c_int, [c_vp, c_int, c_int, C.POINTER(c_int)]),
+    "fate_channel_pump": (c_int, [c_vp]),
+    "fate_channel_wait": (c_int, [c_vp, c_i64, c_vp]),
+    "fate_channel_find": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_int), C.POINTER(c_i64)]),
+    "fate_channel_pending": (c_int, [c_vp, C.POINTER(c_i64), c_int, C.POINTER(c_int), C.POINTER(c_int)]),
     "fate_engine_set_dense": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, C.c_float, C.c_float]),
     "fate_engine_set_dense_layer": (c_int, [c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fate_ffn_decode_timed": (c_int, [c_vp, c_int, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_int,

@@ -35,6 +35,31 @@ def main():
            "csv_rows": [list(r.csv_values()) for r in res.rows[:2]],
            "ablation_stages": [s["stage"] for s in abl["stages"]], "ablation_budget": abl["budget_bytes"],
            "summary_keys": sorted(res.summary["groups"][0].keys())}
+    # _Channel queue semantics (pipeline.py:163-264): random enqueue / promote /
+    # drop_stale sequences and the pending order (seq ids) after every operation
+    import numpy as np
+    from moesim import pipeline as mp
+    rng = np.random.default_rng(11)
+    chans = []
+    for _ in range(60):
+        ch = mp._Channel()
+        ops, states = [], []
+        for _ in range(int(rng.integers(5, 40))):
+            r = rng.random()
+            if r < 0.6:
+                op = ["enqueue", "prefetch" if rng.random() < 0.6 else "ondemand", int(rng.integers(0, 4)),
+                      int(rng.integers(0, 4)), int(rng.integers(0, 8))]
+                ch.enqueue(op[1], op[2], op[3], op[4], 4, 1.0, 0.0)
+            elif r < 0.8:
+                op = ["promote"]
+                ch.promote_ondemand()
+            else:
+                op = ["drop_stale", int(rng.integers(0, 4)), int(rng.integers(0, 4))]
+                ch.drop_stale((op[1], op[2]))
+            ops.append(op)
+            states.append([t.seq for t in ch.pending])
+        chans.append({"ops": ops, "pending": states})
+    out["channel"] = chans
     with open(os.path.join(OUT, "golden_harness.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print("wrote golden_harness.json", len(rows), "rows")
