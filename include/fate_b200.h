@@ -114,6 +114,10 @@ int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets, const uin
  * consumers: full-wait start, full passed, released); then [8][4] cycles of
  * consumer warp 1's first phase-A rows (dots done, sums done, store done). */
 int fate_k3_profile(uint64_t *out_host);
+/* Profiling builds only (FATE_PROF=1): CTA 0's per-stage K4 timeline of the last
+ * up-projection launch, out_host[256*5] (ns): issued, landed, dequantized, MMA saw
+ * full, MMA committed. */
+int fate_k4_profile(uint64_t *out_host);
 /* Diagnostics: phase timestamps of the last K1 launch, out_host[8] ns. */
 int fate_k1_profile(uint64_t *out_host);
 

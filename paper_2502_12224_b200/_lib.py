@@ -84,6 +84,7 @@ SIGNATURES = {
     "fate_gate_forward": (c_int, [c_vp, c_dbl, c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_int, c_dbl, c_vp]),
     "fate_ffn_decode": (c_int, [c_vp, c_int, c_int, C.POINTER(c_vp), C.POINTER(C.c_float), c_vp, c_vp, c_vp]),
     "fate_k3_profile": (c_int, [c_vp]),
+    "fate_k4_profile": (c_int, [c_vp]),
     "fate_engine_set_expert_sources": (c_int, [c_vp, c_int, c_vp]),
     "fate_ipc_get_handle": (c_int, [c_vp, c_vp, C.POINTER(c_i64)]),
     "fate_ipc_open_handle": (c_int, [c_vp, C.POINTER(c_vp)]),

@@ -37,7 +37,9 @@ constexpr int kEpiWarps = 4, kLoadWarps = 8;
 constexpr int kTcThreads = 32 * (kEpiWarps + kLoadWarps + 1);
 constexpr int kMmaWarp = kEpiWarps + kLoadWarps;
 constexpr int kUpStages = 4, kDnStages = 6;  // bf16 operand ring (UMMA layout)
-constexpr int kTileBytes = BM * BK * 2;  // one 128 x 64 bf16 operand tile (16 KB)
+constexpr int kTileBytes = BM * BK * 2;  // one 128 x 64 bf16 weight tile (16 KB)
+constexpr int kXBytes = BN * BK * 2;     // one token / activation tile (16 KB)
+constexpr int kUpStage = 2 * kTileBytes + kXBytes, kDnStage = kTileBytes + kXBytes;
 constexpr int kMaxPrefillExperts = FATE_MAX_EXPERTS + 1;  // routed + shared
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -206,6 +208,23 @@ struct Item {
   int e, tt, rt;  // expert, token tile, row tile
 };
 
+// Profiling builds only (-DFATE_PROF): CTA 0's per-stage timeline of the last
+// up-projection launch: [0] loader passed the slot's empty barrier and issued,
+// [1] loader's copies landed, [2] loader arrived full (dequant done), [3] MMA
+// warp passed full, [4] MMA warp committed (globaltimer ns).
+#ifdef FATE_PROF
+__device__ unsigned long long g_k4_stage[256][5];
+__device__ __forceinline__ unsigned long long k4_time() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K4_STAMP(k, i) \
+  do { if (UP && blockIdx.x == 0 && (k) < 256) g_k4_stage[k][i] = k4_time(); } while (0)
+#else
+#define K4_STAMP(k, i) ((void)0)
+#endif
+
 // Items are expert-major: for e, for token tile, for row tile.
 __device__ __forceinline__ Item item_of(const int *pref, const int *nrt, int n, int idx) {
   // largest e with pref[e] <= idx (binary search; pref is non-decreasing, pref[n] > idx)
@@ -227,7 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                  __nv_bfloat16 *__restrict__ A, float *__restrict__ Z) {
   constexpr int S = UP ? kUpStages : kDnStages;
   constexpr int kLook = S - 2;  // cp.async stages in flight ahead of the dequant (slot reuse waits on the MMA two stages back)
-  constexpr int kStage = UP ? 3 * kTileBytes : 2 * kTileBytes;  // [W1 | W3 | X] or [W2 | A]
+  constexpr int kStage = UP ? kUpStage : kDnStage;  // [W1 | W3 | X] or [W2 | A]
   constexpr uint32_t kAccCols = UP ? 256 : 128;                 // per accumulator buffer
   extern __shared__ __align__(1024) uint8_t smem[];  // S operand stages
   __shared__ PrefillExpert ex[kMaxPrefillExperts];
@@ -391,22 +410,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (ic.it < n_items) {
         bar_wait(&empty[si % S], ((si / S) & 1) ^ 1);
         issue(ic, si);
+        if (lt == 0) K4_STAMP(si, 0);
         ++si;
         next(ic);
       }
       cp_commit();
       cp_wait<kLook>();  // this thread's copies of stage sp have landed
+      if (lt == 0) K4_STAMP(sp, 1);
       dequant(pc, sp);
       // generic-proxy smem writes (cp.async + dequant stores) -> async proxy (tensor core)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&full[sp % S]);
+      if (lt == 0) K4_STAMP(sp, 2);
       next(pc);
     }
     cp_wait<0>();
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer
-    int stage = 0, li = 0;
+    int stage = 0, li = 0, ks = 0;
     uint32_t phase = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
       const Item w = item_of(pref, nrt, n, it);
@@ -421,6 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int k0 = 0; k0 < K; k0 += BK) {
         bar_wait(&full[stage], phase);
         tc_fence_after();
+        if (lane == 0) K4_STAMP(ks, 3);
         if (lane == 0) {
           const uint32_t sb = su32(smem + (size_t)stage * kStage);
           const uint32_t xb = sb + (UP ? 2 : 1) * kTileBytes;
@@ -432,8 +455,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (UP) umma(d0 + 128, smem_desc(sb + kTileBytes + kk * BM * 32, 128, 256), db, idesc, acc);
           }
           umma_commit(&empty[stage]);
+          K4_STAMP(ks, 4);
         }
         __syncwarp();
+        ++ks;
         if (++stage == S) stage = 0, phase ^= 1;
       }
       if (lane == 0) umma_commit(&acc_full[b]);
@@ -490,8 +515,8 @@ K4Dev g_k4[64];
 
 }  // namespace
 
-constexpr size_t kUpSmem = (size_t)kUpStages * 3 * kTileBytes;
-constexpr size_t kDnSmem = (size_t)kDnStages * 2 * kTileBytes;
+constexpr size_t kUpSmem = (size_t)kUpStages * kUpStage;
+constexpr size_t kDnSmem = (size_t)kDnStages * kDnStage;
 
 static cudaError_t k4_device(int *sms) {
   int dev = 0;
@@ -543,3 +568,17 @@ cudaError_t launch_k4_tc(const void *Xb_, int H, const PrefillExpert *ex_dev, in
 }
 
 }  // namespace fate
+
+extern "C" int fate_k4_profile(uint64_t *out_host) {
+#ifdef FATE_PROF
+  if (cudaMemcpyFromSymbol(out_host, fate::g_k4_stage, sizeof(unsigned long long) * 256 * 5) != cudaSuccess) {
+    fate::set_error("fate_k4_profile: copy failed");
+    return FATE_ECUDA;
+  }
+  return FATE_OK;
+#else
+  (void)out_host;
+  fate::set_error("fate_k4_profile: K4 stage stamps are compiled in only with FATE_PROF=1");
+  return FATE_EINVAL;
+#endif
+}

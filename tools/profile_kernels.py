@@ -125,6 +125,26 @@ def k3prof(iters: int):
         torch.cuda.empty_cache()
 
 
+def k4prof(tokens: int):
+    """Profiling build only (FATE_PROF=1): CTA 0's per-stage K4 timeline of the
+    last up-projection launch of an all-resident DeepSeek-shape prefill."""
+    from paper_2502_12224_b200 import _lib
+    prefill(tokens, modes=("allhit",))
+    buf = np.zeros(256 * 5, dtype=np.uint64)
+    _lib.load().fate_k4_profile(buf.ctypes.data)
+    S = buf.reshape(256, 5).astype(np.int64)
+    n = int((S[:, 0] > 0).sum())
+    t0 = S[:n][S[:n] > 0].min()
+    print("stage: issued landed dequantized mma_full mma_committed (us from the first stamp)")
+    for k in range(min(n, 80)):
+        print(f"  {k:3d} " + " ".join(f"{(S[k, i] - t0) / 1e3:8.2f}" if S[k, i] else "       -" for i in range(5)))
+    d = np.diff(S[:n, 4]) / 1e3
+    print(f"per-stage period (commit to commit) median {np.median(d):.3f} us; landed-issued median "
+          f"{np.median((S[:n, 1] - S[:n, 0]) / 1e3):.3f}; dequant {np.median((S[:n, 2] - S[:n, 1]) / 1e3):.3f}; "
+          f"full->commit {np.median((S[:n, 4] - S[:n, 3]) / 1e3):.3f}; arrive->mma saw full "
+          f"{np.median((S[:n, 3] - S[:n, 2]) / 1e3):.3f}")
+
+
 def make_layout_bytes(H, I, bits):
     n = 3 * H * I
     return n * 2 if bits == 16 else n * bits // 8 + n // 64 * 8
@@ -160,7 +180,7 @@ def print_k3_trace(_lib, mhz=1965.0):
               f"C1[{us[1,t,0]:6.2f} {us[1,t,1]:6.2f} {us[1,t,2]:6.2f}] first_full {full_min:6.2f} last_rel {rel_max:6.2f}")
 
 
-def prefill(tokens: int):
+def prefill(tokens: int, modes=("allhit", "cold448")):
     """DeepSeek-MoE-16B shape prefill (BASELINE configs[2]): 28 layers, 64 experts
     top-6 + shared 2 x 1408 (as one 2816 expert, bf16), T tokens; (a) every expert
     resident (pure K4 tensor-core time), (b) 448 INT4 slots cold (the bench case)."""
@@ -175,7 +195,7 @@ def prefill(tokens: int):
     _, g, ch = tr.dense_arrays(cfg)
     gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
     out = {}
-    for mode in ("allhit", "cold448"):
+    for mode in modes:
         if mode == "allhit":
             caps = [64] * 28
         else:
@@ -327,5 +347,5 @@ def allhit(iters: int):
 if __name__ == "__main__":
     mode = sys.argv[1]
     it = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline,
+    {"k3": k3, "allhit": allhit, "k3sweep": k3sweep, "prefill": prefill, "timeline": timeline, "k4prof": k4prof,
      "mixtral": mixtral, "k3prof": k3prof}[mode](it)
