@@ -294,6 +294,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-regimes", action="store_true", help="skip the prefetch / warm-cache decode regimes")
     ap.add_argument("--dense", action="store_true",
                     help="execute the dense part (attention block + shared-expert gate) in the headline run too")
     ap.add_argument("--no-prefill", action="store_true")
@@ -355,8 +356,9 @@ def main():
     dense = dense_w if args.dense else None
     CTX0 = 512
     # -- measured TimingModel -> n (transfer_budget, pipeline.py:151-156)
+    from paper_2502_12224_b200.gatesim import GenConfig as GenConfigFn, gen_trace as gen_trace_fn
     eng = OffloadEngine(cfg, plan.per_layer_capacity, store, weights, P.knobs_for(strategy, plan, 0),
-                        max_tokens=max(T, 64))
+                        max_tokens=max(T, 512))
     if dense is not None:
         eng.set_dense(dense, max_ctx=CTX0 + max(T, 64), ctx0=CTX0)
     cal = eng.decode(gd[:32], chd[:32])
@@ -495,6 +497,62 @@ def main():
                 "k3_ms_per_launch": sum(x["ffn_ms"] for x in pst) / sum(x["steps"] for x in pst)}
         shards.detach(eng)
         shards.close()
+    # -- two more regimes of the same decode: (i) prefetch exercised --
+    # the paper's TimingModel (t_io[4] = 1.6 ms vs 24 ms of compute) gives n = 15, so
+    # every step issues cross-layer INT4 prefetches on the copy streams while K3 runs;
+    # (ii) a warm cache -- decode continues on the cache a 512-token prefill of the
+    # same model left (compare_strategies chaining), so K1 / K3 dominate, not PCIe
+    regimes = {}
+    if not args.no_regimes:
+        paper = P.TimingModel(t_moe=13.0, t_attn=9.0, t_gate=2.0, t_expert_io={16: 6.0, 8: 3.0, 4: 1.6, 2: 0.85})
+        n_p = P.transfer_budget(paper, strategy.prefetch_bits())
+        eng.set_strategy(P.knobs_for(strategy, plan, n_p))
+        pst = []
+        for _ in range(2):
+            eng.reset_cache()
+            pst.append(eng.decode(gd, chd).stats)
+        regimes["prefetch_n15"] = {
+            "tokens_per_s": T * len(pst) / (sum(x["gpu_ms"] for x in pst) / 1e3), "transfer_budget_n": n_p,
+            "prefetch_issued": sum(x["prefetch_issued"] for x in pst) // len(pst),
+            "ondemand_issued": sum(x["ondemand_issued"] for x in pst) // len(pst),
+            "dropped_before_start": sum(x["transfers_dropped"] for x in pst) // len(pst),
+            "h2d_gbs": sum(x["h2d_bytes"] for x in pst) / (sum(x["copy_busy_ms"] for x in pst) * 1e-3) / 1e9,
+            "copy_busy_fraction_of_step": sum(x["copy_busy_ms"] for x in pst) / sum(x["gpu_ms"] for x in pst),
+            "hit_rate_combined": sum(x["cache_hits"] + x["arrival_hits"] for x in pst) / sum(x["accesses"] for x in pst),
+            "what": "paper TimingModel (n = 15): predicted experts of layer l+1 prefetched in INT4 during layer l"}
+        eng.set_strategy(P.knobs_for(strategy, plan, n))
+        pre_tr, _ = gen_trace_fn(cfg, GenConfigFn(seed=rank + 1, num_tokens=512, phase="prefill"), weights=weights)
+        _, gp, chp = pre_tr.dense_arrays(cfg)
+        gpd, chpd = torch.as_tensor(gp, device=dev), torch.as_tensor(chp, device=dev)
+        if eng.max_tokens >= 512:
+            wst = []
+            for _ in range(2):
+                eng.reset_cache()
+                eng.prefill(gpd, chpd, timed=False)
+                wst.append(eng.decode(gd, chd).stats)
+            regimes["warm_after_prefill512"] = {
+                "tokens_per_s": T * len(wst) / (sum(x["gpu_ms"] for x in wst) / 1e3),
+                "hit_rate_cache": sum(x["cache_hits"] for x in wst) / sum(x["accesses"] for x in wst),
+                "k3_ms_per_launch": sum(x["ffn_ms"] for x in wst) / sum(x["steps"] for x in wst),
+                "k1_ms_per_launch": sum(x["gate_ms"] for x in wst) / sum(x["steps"] for x in wst),
+                "h2d_bytes_per_token": sum(x["h2d_bytes"] for x in wst) / (T * len(wst)),
+                "what": "decode on the cache a 512-token prefill of the same model warmed (pipeline.py:828-849)"}
+        del gpd, chpd
+        # (iii) every expert resident (capacity E in every layer, 7.8 GB of INT4 slots):
+        # no transfers at all, the step is K1 + K3 -- the engine's compute floor
+        ares = OffloadEngine(cfg, [cfg.num_experts] * cfg.num_layers, store, weights, P.knobs_for(strategy, plan, n),
+                             max_tokens=max(T, 64))
+        for l in range(cfg.num_layers):
+            ares.seed_resident(l, range(cfg.num_experts))
+        ares.decode(gd[:16], chd[:16])
+        ast_ = [ares.decode(gd, chd).stats for _ in range(2)]
+        regimes["all_resident"] = {
+            "tokens_per_s": T * len(ast_) / (sum(x["gpu_ms"] for x in ast_) / 1e3),
+            "k3_ms_per_launch": sum(x["ffn_ms"] for x in ast_) / sum(x["steps"] for x in ast_),
+            "k3_gbs": sum(x["ffn_bytes"] for x in ast_) / (sum(x["ffn_ms"] for x in ast_) * 1e-3) / 1e9,
+            "k1_ms_per_launch": sum(x["gate_ms"] for x in ast_) / sum(x["steps"] for x in ast_),
+            "what": "every expert resident in INT4 (no transfers): K1 + K3 only"}
+        ares.close()
     # -- the dense part executed: attention block with a K/V cache
     # over a 512-token prompt + Qwen's shared-expert gate in every step; t_attn is then
     # measured instead of assumed, which sets the transfer budget n of this run
@@ -580,6 +638,7 @@ def main():
             "prefill": pre,
             "peer_fetch": peer,
             "dense_part": dense_part,
+            "regimes": regimes,
             "wall_s_timed": wall,
         }
         print(json.dumps(out), flush=True)
