@@ -171,6 +171,11 @@ int fate_engine_set_strategy(fate_engine *eng, const fate_engine_config *cfg);
  * 1 on-demand), step, layer, expert, bits.  counts = {steps, copies}. */
 int fate_engine_timeline(fate_engine *eng, double *step_ms, int max_steps, double *copy_ms, int32_t *copy_meta,
                          int max_copies, int32_t *counts);
+/* Copy timing of timed runs: an event pair around every stride-th transfer only
+ * (default 8; 1 = every transfer, as the timeline of collect_cache_events wants;
+ * 0 = none).  Events between copies delay the copy engine; copy_busy_ms is the
+ * sampled copies' busy time scaled by bytes. */
+int fate_engine_set_copy_timing(fate_engine *eng, int stride);
 
 /* Router weights W[L,E,H] fp64 and temperatures tau[L] (host arrays; copied). */
 int fate_engine_set_gate(fate_engine *eng, const double *W_host, const double *tau_host);

@@ -93,6 +93,7 @@ SIGNATURES = {
     "fate_dense_step": (c_int, [c_int, c_int, c_int, c_int, C.c_float, C.c_float] + [c_vp] * 10 + [c_int]
                         + [c_vp] * 8),
     "fate_host_unregister": (c_int, [c_vp]),
+    "fate_engine_set_copy_timing": (c_int, [c_vp, c_int]),
     "fate_channel_create": (c_int, [c_int, c_int, C.POINTER(c_vp)]),
     "fate_channel_destroy": (c_int, [c_vp]),
     "fate_channel_enqueue": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_i64, C.POINTER(c_i64)]),

@@ -760,6 +760,7 @@ struct fate_engine {
   cudaEvent_t ev_k1 = nullptr, ev_arc = nullptr;
   int max_total_I = 0;
   int prefill_max_tokens = 0;
+  int copy_event_stride = 8;  // time every stride-th copy (0: none); fate_engine_set_copy_timing
   // prefill scratch
   void *pf_block = nullptr;
   std::mutex mu;
@@ -1105,6 +1106,15 @@ extern "C" int fate_ipc_close(void *dev_ptr) {
   return FATE_OK;
 }
 
+extern "C" int fate_engine_set_copy_timing(fate_engine *g, int stride) {
+  if (stride < 0) {
+    set_error("fate_engine_set_copy_timing: stride must be >= 0");
+    return FATE_EINVAL;
+  }
+  g->copy_event_stride = stride;
+  return FATE_OK;
+}
+
 extern "C" int fate_host_register(void *host_ptr, int64_t bytes) {
   if (!host_ptr || bytes <= 0) {
     set_error("fate_host_register: bad arguments");
@@ -1307,7 +1317,7 @@ struct Channel {
   }
   int init_serial() {
     serial = true;
-    sev.resize(g->cfg.max_inflight + 4);
+    sev.resize(g->cfg.max_inflight + 2 * FATE_MAX_TOPK + 4);
     for (auto &e : sev) FATE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int i = (int)sev.size() - 1; i >= 0; --i) sev_free.push_back(i);
     return FATE_OK;
@@ -1315,6 +1325,13 @@ struct Channel {
 
   uint32_t submitted_s[2] = {0u, 0u};
   int next_stream = 0;
+  // Copy timing: an event pair around every stride-th copy only.  Each stream op
+  // between two copies costs the DMA engine ~7 us of the next copy's start, so
+  // timing every copy slowed cold decode by 7 %; the sampled copies' busy time,
+  // scaled by bytes, estimates the channel's busy time (copy_busy_ms).
+  int stride = 8;
+  uint64_t nsub = 0;
+  int64_t sampled_bytes = 0;
 
   // Transfers alternate between two copy streams (two DMA engines), in the
   // channel's FIFO submission order; the completion of each stream is a
@@ -1336,7 +1353,8 @@ struct Channel {
       const auto &tab = g->src_table[t.bits];
       const uint8_t *dsrc = tab.empty() ? nullptr : tab[le];  // expert-sharded mode: device / peer copy
       const uint8_t *src = dsrc ? dsrc : g->host_pool[t.bits] + le * g->host_stride[t.bits];
-      if (timed && !ev_free.empty()) {
+      if (timed && stride > 0 && (nsub++ % (uint64_t)stride) == 0 && !ev_free.empty()) {
+        sampled_bytes += bytes;
         evi = ev_free.back();
         ev_free.pop_back();
         FATE_CUDA(cudaEventRecord(ev[evi], s));
@@ -1347,7 +1365,6 @@ struct Channel {
       // landed marks are read only for queued prefetches (K1's arrival check):
       // on-demand copies skip the extra stream op between back-to-back copies
       if (t.kind == 0 && !serial) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
-      FATE_CUDA(cudaEventRecord(g->xlast[si], s));
       (dsrc ? d2d_bytes : h2d_bytes) += bytes;
     }
     if (serial) {
@@ -1362,6 +1379,8 @@ struct Channel {
     // the step's wait flag is released by the copy streams themselves right
     // after the last transfer the step needs (the host also sets it when reaping)
     if (t.signal_token >= 0) {
+      // everything submitted so far on the other copy stream precedes the flag
+      FATE_CUDA(cudaEventRecord(g->xlast[si ^ 1], si ? g->xstream : g->xstream2));
       FATE_CUDA(cudaStreamWaitEvent(s, g->xlast[si ^ 1], 0));
       FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->ready_dev + t.signal_layer), (uint32_t)t.signal_token + 1u, 0));
     }
@@ -1402,9 +1421,13 @@ struct Channel {
     }
   }
 
+  // Prefetches are submitted at most max_inflight at a time (pending ones stay
+  // reorderable / droppable, as in the reference's queue); on-demand loads at the
+  // front of the queue (promote_ondemand) are urgent and all go to the copy
+  // engines at once, back to back, so no host round trip separates them.
   int pump() {
     reap();
-    while ((int)inflight.size() < g->cfg.max_inflight && !pending.empty()) {
+    while (!pending.empty() && ((int)inflight.size() < g->cfg.max_inflight || pending.front().kind == 1)) {
       Transfer t = pending.front();
       pending.pop_front();
       if (int st = submit_one(t)) return st;
@@ -1449,6 +1472,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   Channel ch;
   ch.g = g;
   ch.timed = timed;
+  ch.stride = g->copy_event_stride;
   if (serial_launches())
     if (int st = ch.init_serial()) return st;
   std::vector<cudaEvent_t> kev;  // per step: K1 start, K1 end, K3 start (after the wait), K3 end
@@ -1458,7 +1482,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     return FATE_EINVAL;
   }
   if (timed) {
-    ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 4));
+    ch.ev.resize(2 * (size_t)(g->cfg.max_inflight + 2 * FATE_MAX_TOPK + 4));
     for (auto &e : ch.ev) FATE_CUDA(cudaEventCreate(&e));
     for (int i = (int)ch.ev.size() - 2; i >= 0; i -= 2) ch.ev_free.push_back(i);
     kev.resize(4 * (size_t)n_steps);
@@ -1715,7 +1739,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   st.transfers_dropped = ch.dropped;
   st.h2d_bytes = ch.h2d_bytes;
   st.d2d_bytes = ch.d2d_bytes;
-  st.copy_busy_ms = ch.copy_ms;
+  // busy time of the sampled copies, scaled to every byte the channel moved
+  st.copy_busy_ms = ch.sampled_bytes > 0 ? ch.copy_ms * (double)(ch.h2d_bytes + ch.d2d_bytes) / (double)ch.sampled_bytes
+                                         : 0.0;
   st.recall_sum = ds.recall_sum;
   st.recall_n = (int64_t)ds.recall_n;
   st.trace_mismatches = (int64_t)ds.mismatches;
@@ -2256,6 +2282,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   Channel ch;
   ch.g = g;
   ch.timed = timed;
+  ch.stride = g->copy_event_stride;
   if (serial_launches())
     if (int st = ch.init_serial()) return st;
   std::vector<cudaEvent_t> kev;
@@ -2532,7 +2559,9 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   st.transfers_dropped = ch.dropped;
   st.h2d_bytes = ch.h2d_bytes;
   st.d2d_bytes = ch.d2d_bytes;
-  st.copy_busy_ms = ch.copy_ms;
+  // busy time of the sampled copies, scaled to every byte the channel moved
+  st.copy_busy_ms = ch.sampled_bytes > 0 ? ch.copy_ms * (double)(ch.h2d_bytes + ch.d2d_bytes) / (double)ch.sampled_bytes
+                                         : 0.0;
   st.recall_sum = ds.recall_sum;
   st.recall_n = (int64_t)ds.recall_n;
   st.trace_mismatches = (int64_t)ds.mismatches;

@@ -105,6 +105,10 @@ class OffloadEngine:
                   "fate_engine_set_dense_layer")
         self.dense = dense  # the engine reads these buffers on every step
 
+    def set_copy_timing(self, stride: int) -> None:
+        """Time every stride-th transfer of timed runs (default 8; 1: every one, 0: none)."""
+        check(self._L.fate_engine_set_copy_timing(self._h, int(stride)), "fate_engine_set_copy_timing")
+
     def set_strategy(self, knobs: StrategyKnobs) -> None:
         c = self._config(knobs)
         check(self._L.fate_engine_set_strategy(self._h, C.byref(c)), "fate_engine_set_strategy")

@@ -317,6 +317,8 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     cache, eng = bind_engine(cache, plan, cfg, gates, experts, knobs, max_tokens=max(len(toks), engine_tokens, 1))
     if dense is not None:
         eng.set_dense(dense, max_ctx=dense_ctx0 + max(len(toks), engine_tokens, 1), ctx0=dense_ctx0)
+    # every transfer in the timeline when the caller collects events, else sampled timing
+    eng.set_copy_timing(1 if collect_cache_events else 8)
     if strategy.kind == "eap" and not _eap_continue:
         eng.reset_eap()
     dev = torch.device("cuda", eng.device)

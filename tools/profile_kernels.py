@@ -239,6 +239,7 @@ def timeline(tokens: int):
     gd, chd = torch.as_tensor(g, device="cuda"), torch.as_tensor(ch, device="cuda")
     eng = OffloadEngine(cfg, plan.per_layer_capacity, store, weights, P.knobs_for(P.Strategy.fate(), plan, 0),
                         max_tokens=max(tokens, 64))
+    eng.set_copy_timing(1)  # every transfer in the timeline
     eng.decode(gd, chd)
     eng.reset_cache()
     res = eng.decode(gd, chd)
