@@ -1386,8 +1386,24 @@ struct Channel {
     }
     ++submitted;
     const uint32_t sseq = ++submitted_s[si];
-    FATE_CU(p_write32((CUstream)s, si ? g->copy_done_dev2 : g->copy_done_dev, sseq, 0));
+    // the stream's completion counter is written once behind the last transfer a
+    // pump() call puts on it (flush_counters): stream ops between back-to-back
+    // copies delay the copy engine; a later counter value also retires the
+    // earlier transfers of the stream (stream order)
+    counter_due[si] = true;
     inflight.push_back(Inflight{submitted, t, evi, si, sseq});
+    return FATE_OK;
+  }
+
+  bool counter_due[2] = {false, false};
+  int flush_counters() {
+    if (serial) return FATE_OK;
+    for (int si = 0; si < 2; ++si)
+      if (counter_due[si]) {
+        counter_due[si] = false;
+        FATE_CU(p_write32((CUstream)(si ? g->xstream2 : g->xstream), si ? g->copy_done_dev2 : g->copy_done_dev,
+                          submitted_s[si], 0));
+      }
     return FATE_OK;
   }
 
@@ -1432,7 +1448,7 @@ struct Channel {
       pending.pop_front();
       if (int st = submit_one(t)) return st;
     }
-    return FATE_OK;
+    return flush_counters();
   }
 
   // promote_ondemand (pipeline.py:241-245): stable partition, on-demand first
