@@ -174,7 +174,10 @@ int fate_engine_timeline(fate_engine *eng, double *step_ms, int max_steps, doubl
 /* Copy timing of timed runs: an event pair around every stride-th transfer only
  * (default 8; 1 = every transfer, as the timeline of collect_cache_events wants;
  * 0 = none).  Events between copies delay the copy engine; copy_busy_ms is the
- * sampled copies' busy time scaled by bytes. */
+ * sampled copies' busy time scaled by bytes.  Decode's per-step kernel events
+ * follow the same stride (max(1, stride); the last step always): gate_ms /
+ * ffn_ms / dense_ms are the sampled steps scaled to all, the timeline's
+ * unsampled steps are NaN. */
 int fate_engine_set_copy_timing(fate_engine *eng, int stride);
 
 /* Router weights W[L,E,H] fp64 and temperatures tau[L] (host arrays; copied). */

@@ -1525,13 +1525,17 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   int launched = 0, processed = 0, k3_next = 0;
   const int lookahead = 4;
   const bool serial = serial_launches();
+  // per-step kernel events only on every stride-th step (and the last): an event
+  // record between K1 and K3 sits on the hand-off path, like a copy's events
+  const int kstride = std::max(1, g->copy_event_stride);
+  auto ksamp = [&](int s) { return timed && (s % kstride == 0 || s == n_steps - 1); };
   // K3 of step s (routed + shared experts), after the step's wait
   auto ffn_step = [&](int s) -> int {
     const int t = s / L, l = s % L;
-    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
+    if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
     FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->k3_scratch, y_dev + ((int64_t)t * L + l) * H, H,
                                        &g->d.stats->ffn_bytes, cs));
-    if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+    if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
     return FATE_OK;
   };
   int status = FATE_OK;
@@ -1577,18 +1581,18 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));  // previous step's ARC update applied
       if (g->dense) {
         // the dense part of (t, l): attention block + shared-expert gate (dense.cu)
-        if (timed) FATE_CUDA(cudaEventRecord(dev_[2 * s], cs));
+        if (ksamp(s)) FATE_CUDA(cudaEventRecord(dev_[2 * s], cs));
         const double *gi = gate_in_dev + ((int64_t)t * L + l) * H;
         if (l == 0) FATE_CUDA(launch_embed(gi, H, g->ds.a, cs));
         FATE_CUDA(launch_dense_step(g->dl[l], g->dd, g->ds.a, l == 0 ? nullptr : y_dev + ((int64_t)t * L + l - 1) * H,
                                     gi, g->ctx0 + t, g->ds, cs));
-        if (timed) FATE_CUDA(cudaEventRecord(dev_[2 * s + 1], cs));
+        if (ksamp(s)) FATE_CUDA(cudaEventRecord(dev_[2 * s + 1], cs));
       }
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
+      if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
       decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
                                                         (volatile uint32_t *)g->ready_dev, t);
       FATE_CHECK_LAUNCH("decode_gate_kernel");
-      if (timed) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
+      if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
       // update_after_layer of this step (pipeline.py:483) on the side stream
       FATE_CUDA(cudaEventRecord(g->ev_k1, cs));
       FATE_CUDA(cudaStreamWaitEvent(g->astream, g->ev_k1, 0));
@@ -1721,8 +1725,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     cudaEventElapsedTime(&ms, t0, kev[4 * (n_steps - 1) + 3]);
     st.gpu_ms = ms;
     double ffn = 0.0, gate = 0.0, dense = 0.0;
-    g->step_ms.resize(4 * (size_t)n_steps);
+    int n_samp = 0;
+    g->step_ms.assign(4 * (size_t)n_steps, std::nan(""));  // unsampled steps stay NaN
     for (int s = 0; s < n_steps; ++s) {
+      if (!ksamp(s)) continue;
+      ++n_samp;
       float t[4] = {0.f, 0.f, 0.f, 0.f};
       for (int j = 0; j < 4; ++j)
         if (s || j || g->dense) cudaEventElapsedTime(&t[j], t0, kev[4 * s + j]);
@@ -1735,9 +1742,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         dense += d;
       }
     }
-    st.ffn_ms = ffn;
-    st.gate_ms = gate;
-    st.dense_ms = dense;
+    // sampled sums scaled to every step
+    const double scale = n_samp ? (double)n_steps / n_samp : 0.0;
+    st.ffn_ms = ffn * scale;
+    st.gate_ms = gate * scale;
+    st.dense_ms = dense * scale;
   }
   if (timed) {
     for (auto &e : ch.ev) cudaEventDestroy(e);
