@@ -179,6 +179,13 @@ int fate_engine_timeline(fate_engine *eng, double *step_ms, int max_steps, doubl
  * ffn_ms / dense_ms are the sampled steps scaled to all, the timeline's
  * unsampled steps are NaN. */
 int fate_engine_set_copy_timing(fate_engine *eng, int stride);
+/* Decode step protocol.  on = 1 (default): K3 is launched right behind K1 and
+ * waits per expert for that expert's copy (a generation mark the copy stream
+ * writes behind it), so the resident experts and the shared expert are computed
+ * while the copies are on PCIe.  on = 0: the compute stream waits for every
+ * copy of the step before K3 starts (K3's event time is then its compute time
+ * alone, which the bench's roofline uses).  Same decisions and results. */
+int fate_engine_set_overlap(fate_engine *eng, int on);
 
 /* Router weights W[L,E,H] fp64 and temperatures tau[L] (host arrays; copied). */
 int fate_engine_set_gate(fate_engine *eng, const double *W_host, const double *tau_host);
@@ -314,6 +321,10 @@ typedef struct fate_run_stats {
   int32_t error; int32_t pad;
   double dense_ms;            /* summed dense-part time (attention block +
                                  shared-expert gate, fate_engine_set_dense)    */
+  double k3_wait_ms;          /* arrival-gated decode: per K3 launch, the
+                                 longest time one of its producer warps waited
+                                 for copies, summed (ffn_ms - k3_wait_ms ~ the
+                                 K3 compute time; 0 with overlap off)          */
 } fate_run_stats;
 
 /* Decode T tokens (simulate_decoding, pipeline.py:343-517).

@@ -63,7 +63,7 @@ class RunStats(C.Structure):
         ("transfers_done", c_i64), ("transfers_dropped", c_i64), ("h2d_bytes", c_i64),
         ("copy_busy_ms", c_dbl), ("recall_sum", c_dbl), ("recall_n", c_i64), ("trace_mismatches", c_i64),
         ("ffn_bytes", c_i64), ("ffn_flops", c_dbl), ("near_ties", c_i64), ("d2d_bytes", c_i64),
-        ("error", C.c_int32), ("pad", C.c_int32), ("dense_ms", c_dbl),
+        ("error", C.c_int32), ("pad", C.c_int32), ("dense_ms", c_dbl), ("k3_wait_ms", c_dbl),
     ]
 
     def as_dict(self) -> dict:
@@ -94,6 +94,7 @@ SIGNATURES = {
                         + [c_vp] * 8),
     "fate_host_unregister": (c_int, [c_vp]),
     "fate_engine_set_copy_timing": (c_int, [c_vp, c_int]),
+    "fate_engine_set_overlap": (c_int, [c_vp, c_int]),
     "fate_channel_create": (c_int, [c_int, c_int, C.POINTER(c_vp)]),
     "fate_channel_destroy": (c_int, [c_vp]),
     "fate_channel_enqueue": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_i64, C.POINTER(c_i64)]),

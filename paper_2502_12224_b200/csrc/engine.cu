@@ -394,11 +394,13 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   const unsigned m_od = __ballot_sync(FULL, odm), m_need = __ballot_sync(FULL, pref);
   const int n_od = __popc(m_od), n_need = __popc(m_need), i_od = __popc(m_od & lt), i_need = __popc(m_need & lt);
   int arr = 0, b = slot_b, src = 16;
+  uint32_t want = 0;  // generation K3 waits for in buffer b (copy still in flight)
   if (hit) src = d.cached_bits < 16 ? d.cached_bits : 16;
   if (pref) {
     b = pend_b;
     src = d.prefetch_bits;
     arr = S.pdone_l[ce] == S.pgen_l[ce];
+    want = S.pgen_l[ce];
     msg->need_e[i_need] = ce;
     msg->need_b[i_need] = b;
   }
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     b = d.free_stack[top - 1 - i_od];
     const uint32_t g = d.buf_gen[b] + 1u;
     d.buf_gen[b] = g;
+    want = g;
     src = d.ondemand_bits;
     d.buf_bits[b] = d.ondemand_bits;
     msg->od_e[i_od] = ce;
@@ -540,12 +543,12 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   FfnBatch &B = *d.batch;
   if (act)
     B.e[lane] = FfnExpert{d.pool + (int64_t)b * d.buf_stride, (float)S.w[ce], d.I, hit ? S.bbits_l[ce] : src,
-                          lane * d.I, 0};
+                          odm || pref ? 1 : 0, odm || (pref && !arr) ? b : -1, want};
   if (lane == 0) {
     int n = k, off = k * d.I;
     if (S.shared_present) {
-      B.e[n] = FfnExpert{d.shared[layer], d.shared_gate ? d.shared_gate[layer] : 1.0f, d.I_shared, d.shared_bits, off,
-                         0};
+      B.e[n] = FfnExpert{d.shared[layer], d.shared_gate ? d.shared_gate[layer] : 1.0f, d.I_shared, d.shared_bits, 0,
+                         -1, 0u};
       off += d.I_shared;
       ++n;
     }
@@ -761,6 +764,7 @@ struct fate_engine {
   int max_total_I = 0;
   int prefill_max_tokens = 0;
   int copy_event_stride = 8;  // time every stride-th copy (0: none); fate_engine_set_copy_timing
+  bool k3_overlap = true;     // decode: K3 launched behind K1, gated per expert on its copy (fate_engine_set_overlap)
   // prefill scratch
   void *pf_block = nullptr;
   std::mutex mu;
@@ -1106,6 +1110,11 @@ extern "C" int fate_ipc_close(void *dev_ptr) {
   return FATE_OK;
 }
 
+extern "C" int fate_engine_set_overlap(fate_engine *g, int on) {
+  g->k3_overlap = on != 0;
+  return FATE_OK;
+}
+
 extern "C" int fate_engine_set_copy_timing(fate_engine *g, int stride) {
   if (stride < 0) {
     set_error("fate_engine_set_copy_timing: stride must be >= 0");
@@ -1310,6 +1319,7 @@ struct Channel {
   // launch-serialised mode: completions are seen through events and every flag
   // is set by this thread (no stream memory operations at all)
   bool serial = false;
+  bool mark_all = false;  // landed marks behind on-demand copies too (arrival-gated K3)
   std::vector<cudaEvent_t> sev;  // one per in-flight slot
   std::vector<int> sev_free;
   ~Channel() {
@@ -1338,12 +1348,34 @@ struct Channel {
   // per-stream counter written behind its copies.  A step's wait flag is
   // written on the stream of the last transfer the step needs, after waiting
   // for the other stream's last copy, so it still follows every one of them.
+  //
+  // A buffer can be released while a copy into it is still running (a prefetch
+  // the gate did not choose is dropped after it started) and be handed to the
+  // next transfer at once.  That transfer goes to the same copy stream as the
+  // running one, so stream order serialises the two writes and their landed
+  // marks (the generation K1 and K3 compare against never goes backwards).
+  std::vector<int> buf_si;        // stream of the last copy into each buffer (-1: none)
+  std::vector<uint32_t> buf_seq;  // its per-stream sequence number
+  int stream_for(int buf) {
+    if ((size_t)buf >= buf_si.size()) buf_si.resize(buf + 1, -1), buf_seq.resize(buf + 1, 0u);
+    const int last = buf_si[buf];
+    if (last >= 0) {
+      if (serial) return last;  // completions are not counted per stream there
+      const uint32_t c = last ? *g->copy_done_host2 : *g->copy_done_host;
+      if ((int32_t)(c - buf_seq[buf]) < 0) return last;  // still in flight
+    }
+    const int si = next_stream;
+    next_stream ^= 1;
+    return si;
+  }
+
   int submit_one(const Transfer &t) {
-    const int si = t.kind == 2 ? 0 : next_stream;
+    const int si = t.kind == 2 ? 0 : stream_for(t.buf);
     const cudaStream_t s = si ? g->xstream2 : g->xstream;
     int evi = -1;
     if (t.kind != 2) {
-      next_stream ^= 1;
+      buf_si[t.buf] = si;
+      buf_seq[t.buf] = submitted_s[si] + 1u;  // the sseq this submission gets below
       if (!g->host_pool[t.bits]) {
         set_error("no pinned host pool registered for a requested bit width");
         return FATE_EINVAL;
@@ -1362,9 +1394,11 @@ struct Channel {
       FATE_CUDA(cudaMemcpyAsync(g->pool + (int64_t)t.buf * g->buf_stride, src, bytes,
                                 dsrc ? cudaMemcpyDefault : cudaMemcpyHostToDevice, s));
       if (evi >= 0) FATE_CUDA(cudaEventRecord(ev[evi + 1], s));
-      // landed marks are read only for queued prefetches (K1's arrival check):
-      // on-demand copies skip the extra stream op between back-to-back copies
-      if (t.kind == 0 && !serial) FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
+      // landed marks: K1's arrival check of queued prefetches and, in the
+      // arrival-gated decode, K3's per-expert gate (a write-value op behind a
+      // copy does not delay the next one; an event record does)
+      if ((t.kind == 0 || mark_all) && !serial)
+        FATE_CU(p_write32((CUstream)s, (CUdeviceptr)(g->d.buf_done + t.buf), t.gen, 0));
       (dsrc ? d2d_bytes : h2d_bytes) += bytes;
     }
     if (serial) {
@@ -1525,17 +1559,39 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   int launched = 0, processed = 0, k3_next = 0;
   const int lookahead = 4;
   const bool serial = serial_launches();
-  // per-step kernel events only on every stride-th step (and the last): an event
-  // record between K1 and K3 sits on the hand-off path, like a copy's events
+  // arrival-gated K3: launched right behind K1 (after the step's ARC update),
+  // each expert's pieces start once its copy landed, so K3 works through the
+  // resident experts while the copies are still on PCIe
+  // (not with device-memory sources, expert-sharded mode: a device-to-device
+  // cudaMemcpyAsync may run as a copy kernel, which a waiting K3 holding every
+  // SM would never let start)
+  bool dev_src = false;
+  for (const auto &tab : g->src_table) dev_src = dev_src || !tab.empty();
+  const bool overlap = g->k3_overlap && !serial && !dev_src;
+  ch.mark_all = overlap;
+  // per-step kernel events only on every layer of every stride-th token (and the
+  // last step): an event record between K1 and K3 sits on the hand-off path, like
+  // a copy's events; whole tokens keep every layer equally represented
   const int kstride = std::max(1, g->copy_event_stride);
-  auto ksamp = [&](int s) { return timed && (s % kstride == 0 || s == n_steps - 1); };
+  auto ksamp = [&](int s) { return timed && ((s / L) % kstride == 0 || s == n_steps - 1); };
   // K3 of step s (routed + shared experts), after the step's wait
+  // FATE_HOSTPROF: host time spent in the launch calls (diagnostics)
+  const bool hprof = getenv("FATE_HOSTPROF") != nullptr;
+  double h_k3 = 0.0, h_k3max = 0.0, h_front = 0.0, h_frontmax = 0.0, h_msg = 0.0;
+  auto hnow = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   auto ffn_step = [&](int s) -> int {
     const int t = s / L, l = s % L;
+    const double h0 = hprof ? hnow() : 0.0;
     if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 2], cs));
     FATE_CUDA(launch_ffn_decode_engine(g->d.batch, g->d.x, g->k3_scratch, y_dev + ((int64_t)t * L + l) * H, H,
-                                       &g->d.stats->ffn_bytes, cs));
+                                       &g->d.stats->ffn, overlap ? g->d.buf_done : nullptr,
+                                       overlap ? (const volatile uint32_t *)g->ready_dev : nullptr, cs));
     if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 3], cs));
+    if (hprof) {
+      const double d = hnow() - h0;
+      h_k3 += d;
+      h_k3max = std::max(h_k3max, d);
+    }
     return FATE_OK;
   };
   int status = FATE_OK;
@@ -1575,6 +1631,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     // enqueue compute for steps up to `lookahead` beyond the host's progress
     while (launched < n_steps && launched < processed + (serial ? 1 : lookahead) && (!serial || k3_next == launched)) {
       const int s = launched, t = s / L, l = s % L;
+      const double hf0 = hprof ? hnow() : 0.0;
       // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
       // tail block + router rows of W_l (and W_{l+1} when predicting)
       const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
@@ -1600,18 +1657,27 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       FATE_CHECK_LAUNCH("arc_update_kernel (step update)");
       FATE_CUDA(cudaEventRecord(g->ev_arc, g->astream));
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
-      // serial mode: no stream wait at all (the host enqueues K3 only once the flag is set)
-      if (!serial)
+      // serial mode: no stream wait at all (the host enqueues K3 only once the flag is set);
+      // arrival-gated: K3 itself waits per expert, behind this step's ARC update
+      // (K3 holds every SM while it waits, the update must not queue behind it)
+      if (overlap) FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));
+      else if (!serial)
         FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u, CU_STREAM_WAIT_VALUE_GEQ));
       if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
       if (!serial && (status = ffn_step(s))) break;
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K3 step %d\n", s);
       ++launched;
+      if (hprof) {
+        const double d = hnow() - hf0;
+        h_front += d;
+        h_frontmax = std::max(h_frontmax, d);
+      }
     }
     // service the step message of the next unprocessed step
     StepMsg &m = g->ring_host[processed % kRing];
     if (m.seq == (uint32_t)processed + 1u) {
       std::atomic_thread_fence(std::memory_order_acquire);
+      const double hm0 = hprof ? hnow() : 0.0;
       const int t = m.token, l = m.layer;
       // drop queued prefetches for this step that the gate did not choose
       for (int i = 0; i < m.n_drop; ++i) {
@@ -1631,7 +1697,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       for (int i = 0; i < m.n_od; ++i)
         ch.pending.push_back(Transfer{1, t, l, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
       ch.promote();
-      if (!m.self_signaled) {
+      if (!m.self_signaled && !overlap) {
         // the compute stream may proceed once every needed transfer landed:
         // attach the signal to the last needed one still queued, else signal
         // behind everything already submitted.
@@ -1655,6 +1721,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
                 ch.inflight.size());
       ++processed;
       last_progress = std::chrono::steady_clock::now();
+      if ((status = ch.pump())) break;
+      if (hprof) h_msg += hnow() - hm0;
     }
     if ((status = ch.pump())) break;
     if (m.seq != (uint32_t)processed + 1u) {
@@ -1678,6 +1746,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
     std::atomic_thread_fence(std::memory_order_seq_cst);
   }
+  if (hprof)
+    fprintf(stderr, "[fate] host us/step: launch block %.2f (max %.1f) of which K3 launch %.2f (max %.1f); "
+            "message service + submit %.2f\n", h_front / n_steps, h_frontmax, h_k3 / n_steps, h_k3max, h_msg / n_steps);
   if (getenv("FATE_DEBUG"))
     fprintf(stderr, "[fate] decode loop exit status=%d processed=%d/%d pending=%zu inflight=%zu err=%s\n", status,
             processed, n_steps, ch.pending.size(), ch.inflight.size(), g_err.c_str());
@@ -1771,7 +1842,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   st.recall_n = (int64_t)ds.recall_n;
   st.trace_mismatches = (int64_t)ds.mismatches;
   st.near_ties = (int64_t)ds.near_ties;
-  st.ffn_bytes = (int64_t)ds.ffn_bytes;
+  st.ffn_bytes = (int64_t)ds.ffn.bytes;
+  st.k3_wait_ms = ds.ffn.wait_ns * 1e-6;
   st.error = status;
   if (stats) *stats = st;
   return status;

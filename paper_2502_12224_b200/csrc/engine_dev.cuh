@@ -55,7 +55,8 @@ struct Ctrl {
 
 struct DevStats {
   unsigned long long accesses, cache_hits, arrival_hits, dequant_count, prefetch_issued, ondemand_issued;
-  unsigned long long mismatches, near_ties, recall_n, ffn_bytes;
+  unsigned long long mismatches, near_ties, recall_n;
+  FfnStats ffn;
   double recall_sum;
 };
 

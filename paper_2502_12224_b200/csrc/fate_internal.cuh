@@ -105,9 +105,12 @@ struct FfnExpert {
   float weight;
   int I;
   int bits;
-  int a_off;           // offset of this expert's rows in the step's concatenated intermediate dim
-  int pad;
+  int late;            // 1: the buffer is filled during this step (on-demand / prefetched), so K3
+                       // orders its units after the others (decided by the schedule, not by timing)
+  int slot;            // >= 0: the buffer is still being filled; K3 reads it once landed[slot] reaches want
+  uint32_t want;       // (the copy's generation, written by the copy stream behind the copy)
 };
+static_assert(sizeof(FfnExpert) == 32, "FfnExpert layout");
 
 constexpr int kMaxFfnExperts = FATE_MAX_TOPK + 2;
 
@@ -127,8 +130,20 @@ static_assert(sizeof(FfnBatch) % 16 == 0, "K3 copies the batch with 16-byte load
 // one stream).  The batch is in DEVICE memory.
 cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
                               cudaStream_t s);
+// K3 counters in device memory: algorithmic bytes, and (arrival-gated mode)
+// the time the most-delayed producer warp of each launch spent waiting for
+// copies, summed over launches (wait_cur: the running launch's maximum)
+struct FfnStats {
+  unsigned long long bytes, wait_ns, wait_cur;
+};
+
+// landed (device memory, per staging buffer) / abort (host-mapped; 0x7FFFFFFF
+// releases every wait): the engine's arrival-gated mode, where K3 is launched
+// right behind K1 and each expert's pieces start once its copy landed; both
+// null = every buffer is complete at launch.
 cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev,
-                                     int H, unsigned long long *bytes_stat, cudaStream_t s);
+                                     int H, FfnStats *stat, const uint32_t *landed,
+                                     const volatile uint32_t *abort, cudaStream_t s);
 cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s);
 size_t ffn_xlay_floats(int H);
 size_t ffn_scratch_bytes(int H);

@@ -235,12 +235,17 @@ struct ExpertPlan {
   float cost;           // weighted bytes of one unit (balancing only)
 };
 
+constexpr int kMaxQList = 32;
+
 struct Plan {
   ExpertPlan ep[kMaxFfnExperts];
   int nq, ns;           // quantized units (round-robin), bf16 units (filled)
   int q_first;          // this CTA's quantized units: q_first, q_first + G, ...
   int nq_mine;
   int s_lo, s_hi;       // this CTA's bf16 units [s_lo, s_hi)
+  int nq_open;          // of those quantized units, the ones whose expert is complete at launch
+  int qreord;           // qlist holds the order (arrival-gated experts last); 0: identity
+  uint8_t qlist[kMaxQList];  // position -> m (this CTA's m-th quantized unit)
 };
 
 struct TileMeta {
@@ -310,6 +315,8 @@ __device__ __noinline__ float share_prefix(int c, int r, float sA, float sB) {
 // Warp 0: the assignment in O(1) per CTA (every CTA derives the same one).
 // Quantized units go round-robin; bf16 units fill every CTA to the same
 // weighted byte count (quantized unit cost = the batch's average).
+__device__ __forceinline__ bool gated(const FfnExpert &e, bool gate) { return gate && e.slot >= 0; }
+
 __device__ void make_plan(const FfnBatch &b, Plan &p, int G, int c, int lane) {
   if (lane < b.n) expert_plan(b.e[lane], b.H, p.ep[lane]);
   __syncwarp();
@@ -333,18 +340,78 @@ __device__ void make_plan(const FfnBatch &b, Plan &p, int G, int c, int lane) {
     p.s_lo = c == 0 ? 0 : min(ns, (int)rintf(__fmul_rn(share_prefix(c, r, sA, sB), scale)));
     p.s_hi = c == G - 1 ? ns : min(ns, (int)rintf(__fmul_rn(share_prefix(c + 1, r, sA, sB), scale)));
     if (p.s_hi < p.s_lo) p.s_hi = p.s_lo;
+    // experts whose buffer is filled during this step go last in the CTA's
+    // sequence, so the units that can run at once are not queued behind a copy
+    // (arrival-gated mode).  The order depends on the schedule only, never on
+    // which copies happen to be in flight, and is the same in both protocols:
+    // y's summation order, hence every bit of y, is timing independent.
+    p.nq_open = p.nq_mine;
+    p.qreord = 0;
+    bool any = false;
+    for (int j = 0; j < b.n; ++j) any = any || (b.e[j].late && b.e[j].bits != 16);
+    if (any && p.nq_mine <= kMaxQList) {
+      int no = 0, n = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int m = 0; m < p.nq_mine; ++m) {
+          int j, s;
+          unit_of(b, p, true, c + m * G, j, s);
+          if ((b.e[j].late != 0) == (pass == 1)) p.qlist[n++] = (uint8_t)m;
+          if (pass == 0) no = n;
+        }
+      p.nq_open = no;
+      p.qreord = no < p.nq_mine;
+    }
   }
   __syncwarp();
 }
 
 // The k-th unit of this CTA's sequence: quantized and bf16 units interleaved
 // evenly (compute-heavy and streaming units overlap in the ring).
+// Arrival-gated quantized units follow all the others.
 __device__ __forceinline__ void my_unit(const FfnBatch &b, const Plan &p, int G, int k, int &j, int &s) {
-  const int nq = p.nq_mine, ns = p.s_hi - p.s_lo, m = nq + ns;
+  const int nq = p.nq_open, ns = p.s_hi - p.s_lo, m = nq + ns;
+  auto quant = [&](int pos) { unit_of(b, p, true, p.q_first + (p.qreord ? p.qlist[pos] : pos) * G, j, s); };
+  if (k >= m) {
+    quant(k - ns);
+    return;
+  }
   // quantized unit number floor((k+1)*nq/m) - 1 sits at position k iff the count steps
   const int before = (int)((long long)k * nq / m), after = (int)((long long)(k + 1) * nq / m);
-  if (after > before) unit_of(b, p, true, p.q_first + before * G, j, s);
+  if (after > before) quant(before);
   else unit_of(b, p, false, p.s_lo + (k - before), j, s);
+}
+
+// Arrival gate (producer warps): the copy filling expert j's buffer has landed
+// (the copy stream writes landed[slot] = generation behind it).  The host's
+// watchdog releases a stuck wait through the abort word.
+__device__ __forceinline__ unsigned long long gclock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// waited: this warp's total wait so far (ns), published as a running maximum
+__device__ __forceinline__ void wait_landed(const FfnExpert &e, const uint32_t *landed, const volatile uint32_t *abort,
+                                            int lane, unsigned long long &waited, FfnStats *stat) {
+  if (lane == 0) {
+    uint32_t v;
+    unsigned long long t0 = 0;
+    for (unsigned n = 1;; ++n) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(landed + e.slot) : "memory");
+      if ((int)(v - e.want) >= 0) break;
+      if (n == 1) t0 = gclock();
+      if ((n & 1023u) == 0 && abort && *abort == 0x7FFFFFFFu) break;
+      // back off: hundreds of pollers on one L2 line slow the copies landing in that slice
+      __nanosleep(256);
+    }
+    if (t0) {
+      waited += gclock() - t0;
+      if (stat) atomicMax(&stat->wait_cur, waited);
+    }
+    // the bulk copies that follow read the buffer through the async proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
 }
 
 // x laid out for every width: slot s (chunk width cols = 8, 16, 32, 64
@@ -573,7 +640,8 @@ template <int HT>
 __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__restrict__ batch_p,
                                                           const float4 *__restrict__ xlay, float *__restrict__ part,
                                                           unsigned int *__restrict__ bar, float *__restrict__ y,
-                                                          unsigned long long *bytes_stat, int stages) {
+                                                          FfnStats *stat, const uint32_t *__restrict__ landed,
+                                                          const volatile uint32_t *abort, int stages) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ FfnBatch batch;
   __shared__ Plan plan;
@@ -623,10 +691,10 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       const uint32_t xbytes = (uint32_t)(4 * lay_stride * 16);
       mbar_expect_tx(&x_bar, xbytes);
       bulk_g2s(xl, xlay, xbytes, &x_bar);
-      if (blockIdx.x == 0 && bytes_stat) {
+      if (blockIdx.x == 0 && stat) {
         unsigned long long bytes = 0;
         for (int j = 0; j < batch.n; ++j) bytes += make_layout(H, batch.e[j].I, batch.e[j].bits).payload;
-        atomicAdd(bytes_stat, bytes);
+        atomicAdd(&stat->bytes, bytes);
       }
     }
     const int np = kProducers < stages - 1 ? kProducers : stages - 1;
@@ -666,10 +734,20 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       }
     };
     int pj = -1, ps = 0;
+    uint32_t open = 0;  // experts known landed (arrival-gated mode)
+    unsigned long long waited = 0;
     for (int k = 0; k < n_units; ++k) {
       int j, s;
       my_unit(batch, plan, G, k, j, s);
       const FfnExpert &ex = batch.e[j];
+      if (gated(ex, landed != nullptr) && !((open >> j) & 1u)) {
+        // finish the previous unit before possibly waiting (its W-pieces would
+        // otherwise sit behind this unit's A-pieces), then wait for the copy
+        if (pj >= 0) issue_w(k - 1, pj, ps);
+        pj = -1;
+        wait_landed(ex, landed, abort, lane, waited, stat);
+        open |= 1u << j;
+      }
       const ExpertPlan &ep = plan.ep[j];
       const int bits = ex.bits;
       const Layout Lo = make_layout(H, ex.I, bits);
@@ -788,6 +866,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     K3_PROF(4);
     grid_barrier(bar);
     K3_PROF(5);
+    // every producer's waits preceded stages its CTA consumed before the barrier
+    if (blockIdx.x == 0 && stat && landed) {
+      stat->wait_ns += *(volatile unsigned long long *)&stat->wait_cur;
+      stat->wait_cur = 0;
+    }
   }
   consumer_sync();
   // rows [r0, r0 + nrow) of y: thread (g, r) sums the CTAs c = g, g + ng, ... of row r,
@@ -892,11 +975,12 @@ cudaError_t launch_build_xlay(const float *x, int H, float *xlay, cudaStream_t s
 
 cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
                               cudaStream_t s) {
-  return launch_ffn_decode_engine(batch_dev, xlay, scratch, y_dev, H, nullptr, s);
+  return launch_ffn_decode_engine(batch_dev, xlay, scratch, y_dev, H, nullptr, nullptr, nullptr, s);
 }
 
 cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xlay, void *scratch, float *y_dev, int H,
-                                     unsigned long long *bytes_stat, cudaStream_t s) {
+                                     FfnStats *stat, const uint32_t *landed,
+                                     const volatile uint32_t *abort, cudaStream_t s) {
   int sms = 0;
   cudaError_t e = device_info(&sms);
   if (e != cudaSuccess) return e;
@@ -920,9 +1004,9 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (H == 2048) return cudaLaunchKernelEx(&cfg, ffn_kernel<2048>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
-  if (H == 4096) return cudaLaunchKernelEx(&cfg, ffn_kernel<4096>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
-  return cudaLaunchKernelEx(&cfg, ffn_kernel<0>, batch_dev, xl, part, bar, y_dev, bytes_stat, st);
+  if (H == 2048) return cudaLaunchKernelEx(&cfg, ffn_kernel<2048>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
+  if (H == 4096) return cudaLaunchKernelEx(&cfg, ffn_kernel<4096>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
+  return cudaLaunchKernelEx(&cfg, ffn_kernel<0>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
 }
 
 }  // namespace fate
@@ -966,7 +1050,7 @@ extern "C" int fate_ffn_decode(const float *x_dev, int H, int n, const uint8_t *
       set_error("fate_ffn_decode: buffer header does not describe a packed expert of this hidden size");
       return FATE_EINVAL;
     }
-    b.e[j] = FfnExpert{bufs[j], weights[j], h.I, h.bits, off, 0};
+    b.e[j] = FfnExpert{bufs[j], weights[j], h.I, h.bits, 0, -1, 0u};
     off += h.I;
   }
   b.total_I = off;
@@ -1014,7 +1098,7 @@ extern "C" int fate_ffn_decode_timed(const float *x_dev, int H, int n, int nsets
         set_error("fate_ffn_decode_timed: buffer header does not describe a packed expert of this hidden size");
         return FATE_EINVAL;
       }
-      b.e[j] = FfnExpert{buf, weights[j], h.I, h.bits, off, 0};
+      b.e[j] = FfnExpert{buf, weights[j], h.I, h.bits, 0, -1, 0u};
       off += h.I;
     }
     b.total_I = off;

@@ -109,6 +109,11 @@ class OffloadEngine:
         """Time every stride-th transfer of timed runs (default 8; 1: every one, 0: none)."""
         check(self._L.fate_engine_set_copy_timing(self._h, int(stride)), "fate_engine_set_copy_timing")
 
+    def set_overlap(self, on: bool) -> None:
+        """Decode: K3 launched behind K1 and gated per expert on its copy (default),
+        or the compute stream waits for all of a step's copies first."""
+        check(self._L.fate_engine_set_overlap(self._h, int(bool(on))), "fate_engine_set_overlap")
+
     def set_strategy(self, knobs: StrategyKnobs) -> None:
         c = self._config(knobs)
         check(self._L.fate_engine_set_strategy(self._h, C.byref(c)), "fate_engine_set_strategy")

@@ -317,8 +317,11 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     cache, eng = bind_engine(cache, plan, cfg, gates, experts, knobs, max_tokens=max(len(toks), engine_tokens, 1))
     if dense is not None:
         eng.set_dense(dense, max_ctx=dense_ctx0 + max(len(toks), engine_tokens, 1), ctx0=dense_ctx0)
-    # every transfer in the timeline when the caller collects events, else sampled timing
+    # every transfer and kernel in the timeline when the caller collects events (and
+    # K3 waits for a step's copies on the stream, so its events are compute alone),
+    # else sampled timing and the arrival-gated K3 (engine.OffloadEngine.set_overlap)
     eng.set_copy_timing(1 if collect_cache_events else 8)
+    eng.set_overlap(not collect_cache_events)
     if strategy.kind == "eap" and not _eap_continue:
         eng.reset_eap()
     dev = torch.device("cuda", eng.device)
@@ -329,12 +332,18 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
         _warn_mismatch(st)
     L = cfg.num_layers
     events = []
-    stall = 0.0
+    stall, timed_steps = 0.0, 0
     for s, (g0, g1, m0, m1) in enumerate(res.step_ms):
+        if np.isnan(g1):
+            continue  # sampled timing: this step carried no events
+        timed_steps += 1
         t, l = toks[s // L], s % L
         events.append(TimelineEvent(g0, g1, "compute", f"gate t{t} L{l}"))
         events.append(TimelineEvent(m0, m1, "compute", f"moe t{t} L{l}"))
         stall += max(0.0, m0 - g1)
+    # stall: the compute stream's waits between K1 and K3 (scaled from the timed
+    # steps) plus, arrival-gated, the time K3 itself waited for copies
+    stall = stall * (len(res.step_ms) / timed_steps if timed_steps else 0.0) + st.get("k3_wait_ms", 0.0)
     kinds = {0: "prefetch", 1: "ondemand"}
     for (c0, c1, kind, step, layer, expert, bits) in res.copies:
         if kind in kinds:
@@ -471,5 +480,7 @@ def measure_timing_model(engine_result_stats: dict, cfg: ModelConfig, steps: int
     t_io = {b: float(np.median(v)) for b, v in io.items()}
     if engine_result_stats.get("dense_ms", 0.0) > 0:
         t_attn_ms = engine_result_stats["dense_ms"] / steps
-    return TimingModel(t_moe=engine_result_stats["ffn_ms"] / steps, t_attn=t_attn_ms,
+    # K3's event time less the time it waited for copies (arrival-gated decode)
+    t_moe = (engine_result_stats["ffn_ms"] - engine_result_stats.get("k3_wait_ms", 0.0)) / steps
+    return TimingModel(t_moe=t_moe, t_attn=t_attn_ms,
                        t_gate=engine_result_stats["gate_ms"] / steps, t_expert_io=t_io, dequant_ms=0.0)

@@ -215,3 +215,30 @@ def test_expert_sharded_sources_same_decisions_and_outputs(name):
     assert back.stats["d2d_bytes"] == 0 and back.stats["h2d_bytes"] > 0
     shards.close()
     eng.close()
+
+
+@pytest.mark.parametrize("name,n", [("qwen", 15), ("qwen", 0), ("mixtral", 15)])
+def test_arrival_gated_k3_same_decisions_and_outputs(name, n):
+    # the default decode protocol launches K3 right behind K1 and gates each
+    # expert on its copy's generation mark; the stream-wait protocol starts K3
+    # once every copy of the step landed.  Decisions, ARC state and every output
+    # bit must be identical (prefetched experts still in flight included, n = 15)
+    import torch
+    cfg, dec, pre, w, store, eng = _engine(name, n=n, shared=512 if name == "qwen" else 0)
+    gd, chd, g, ch = _dev_trace(dec, cfg)
+    T = min(gd.shape[0], 24)
+    eng.set_overlap(False)
+    ref = eng.decode(gd[:T], chd[:T], want_logs=True)
+    ref_arcs = [eng.arc_state(l) for l in range(cfg.num_layers)]
+    assert ref.stats["k3_wait_ms"] == 0.0
+    eng.set_overlap(True)
+    eng.reset_cache()
+    got = eng.decode(gd[:T], chd[:T], want_logs=True)
+    for a, b in zip(got.logs, ref.logs):
+        assert (a["chosen"], a.get("pred"), a.get("prefetch"), a["hits"], a["ondemand"], a["victims"],
+                a["src_bits"]) == \
+               (b["chosen"], b.get("pred"), b.get("prefetch"), b["hits"], b["ondemand"], b["victims"], b["src_bits"])
+    assert torch.equal(got.y, ref.y)
+    assert [eng.arc_state(l) for l in range(cfg.num_layers)] == ref_arcs
+    assert got.stats["ondemand_issued"] > 0 and got.stats["k3_wait_ms"] > 0.0
+    eng.close()
