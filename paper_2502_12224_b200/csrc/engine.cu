@@ -176,6 +176,10 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
 // [0] block 0 start, [1] tail start, [2] state staged, [3] routed, [4] split,
 // [5] predicted, [6] message posted
 __device__ unsigned long long g_k1_prof[16];
+// FATE_PROF accumulators over a run: [0] sum(K3 end -> K1 block 0 start), [1] n,
+// [2] sum(K1 block 0 start -> message posted), [3] n
+__device__ unsigned long long g_k1_acc[4];
+__device__ unsigned long long g_k1_t0;
 #ifdef FATE_PROF
 #define K1_STAMP(i) (g_k1_prof[i] = gtime1())
 #else
@@ -225,7 +229,15 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) K1_STAMP(0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    K1_STAMP(0);
+#ifdef FATE_PROF
+    // previous K3's end -> this launch (both globaltimer)
+    const unsigned long long e = d.stats->ffn.end_ns, now = gtime1();
+    if (e && now > e) g_k1_acc[0] += now - e, g_k1_acc[1] += 1;
+    g_k1_t0 = now;
+#endif
+  }
   if (threadIdx.x == 0 && blockIdx.x == 1) K1_STAMP(10);
   if (blockIdx.x > 0) {
     // ---- fp64 router row: each thread sums a fixed strided subset, fixed tree
@@ -585,6 +597,10 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (layer == L - 1) C.next_token = token + 1;
     K1_STAMP(6);
     K1_STAMP(7);
+#ifdef FATE_PROF
+    g_k1_acc[2] += gtime1() - g_k1_t0;
+    g_k1_acc[3] += 1;
+#endif
   }
 }
 
@@ -1746,9 +1762,23 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     for (int l = 0; l < L; ++l) g->ready_host[l] = 0x7FFFFFFFu;
     std::atomic_thread_fence(std::memory_order_seq_cst);
   }
-  if (hprof)
+  if (hprof) {
     fprintf(stderr, "[fate] host us/step: launch block %.2f (max %.1f) of which K3 launch %.2f (max %.1f); "
             "message service + submit %.2f\n", h_front / n_steps, h_frontmax, h_k3 / n_steps, h_k3max, h_msg / n_steps);
+    cudaStreamSynchronize(cs);
+    DevStats dsp{};
+    cudaMemcpy(&dsp, g->d.stats, sizeof(dsp), cudaMemcpyDeviceToHost);
+    unsigned long long acc[4] = {0, 0, 0, 0};
+#ifdef FATE_PROF
+    cudaMemcpyFromSymbol(acc, g_k1_acc, sizeof(acc));
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_k1_acc, z, sizeof(z));
+#endif
+    fprintf(stderr, "[fate] device us/step: K3 tail after its last gate opened %.2f (%llu launches waited); "
+            "K3 end -> K1 block start %.2f; K1 block start -> message posted %.2f (profiling builds)\n",
+            dsp.ffn.tail_n ? dsp.ffn.tail_ns * 1e-3 / dsp.ffn.tail_n : 0.0, dsp.ffn.tail_n,
+            acc[1] ? acc[0] * 1e-3 / acc[1] : 0.0, acc[3] ? acc[2] * 1e-3 / acc[3] : 0.0);
+  }
   if (getenv("FATE_DEBUG"))
     fprintf(stderr, "[fate] decode loop exit status=%d processed=%d/%d pending=%zu inflight=%zu err=%s\n", status,
             processed, n_steps, ch.pending.size(), ch.inflight.size(), g_err.c_str());

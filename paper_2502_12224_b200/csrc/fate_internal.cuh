@@ -135,6 +135,10 @@ cudaError_t launch_ffn_decode(const FfnBatch *batch_dev, const float *xlay, void
 // copies, summed over launches (wait_cur: the running launch's maximum)
 struct FfnStats {
   unsigned long long bytes, wait_ns, wait_cur;
+  // diagnostics (globaltimer ns): the running launch's last gate opening, the
+  // summed time from it to the launch's end (the K3 work left after the last
+  // copy landed) and how many launches waited; the last launch's end
+  unsigned long long open_max, tail_ns, tail_n, end_ns;
 };
 
 // landed (device memory, per staging buffer) / abort (host-mapped; 0x7FFFFFFF

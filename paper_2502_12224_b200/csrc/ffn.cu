@@ -405,8 +405,12 @@ __device__ __forceinline__ void wait_landed(const FfnExpert &e, const uint32_t *
       __nanosleep(256);
     }
     if (t0) {
-      waited += gclock() - t0;
-      if (stat) atomicMax(&stat->wait_cur, waited);
+      const unsigned long long t1 = gclock();
+      waited += t1 - t0;
+      if (stat) {
+        atomicMax(&stat->wait_cur, waited);
+        atomicMax(&stat->open_max, t1);
+      }
     }
     // the bulk copies that follow read the buffer through the async proxy
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -903,6 +907,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     }
   }
   if (ctid == 0) K3_PROF(6);
+  if (blockIdx.x == 0 && ctid == 0 && stat) {
+    // CTA 0's rows are its last work; the other CTAs finish theirs within ~1 us
+    const unsigned long long t = gclock(), o = *(volatile unsigned long long *)&stat->open_max;
+    if (landed && o) {
+      stat->tail_ns += t - o;
+      stat->tail_n += 1;
+      stat->open_max = 0;
+    }
+    stat->end_ns = t;
+  }
 }
 
 struct DevInfo {
