@@ -18,6 +18,14 @@ from . import _lib
 from ._lib import EngineConfig, PrefillLog, RunStats, StepLog, check, ptr
 from .core import ModelConfig
 from .errors import InvalidConfig
+
+
+def overlap_default() -> bool:
+    """The decode step protocol engines start with: arrival-gated K3 unless
+    FATE_OVERLAP=0.  A waiting K3 holds every SM of its GPU, so processes that
+    time-share one GPU (more ranks than devices) should use the stream wait."""
+    import os
+    return os.environ.get("FATE_OVERLAP", "1") != "0"
 from .experts import ExpertStore
 
 
@@ -64,6 +72,7 @@ class OffloadEngine:
         h = C.c_void_p()
         check(self._L.fate_engine_create(C.byref(c), C.byref(h)), "fate_engine_create")
         self._h = h
+        self.set_overlap(overlap_default())
         W = np.ascontiguousarray(np.stack([np.asarray(m, np.float64) for m in weights.matrices]))
         tau = np.ascontiguousarray(np.asarray(weights.temperatures, np.float64))
         if W.shape != (cfg.num_layers, cfg.num_experts, cfg.hidden_dim):

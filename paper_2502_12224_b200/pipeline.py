@@ -321,7 +321,8 @@ def simulate_decoding(trace: GateTrace, strategy: Strategy, plan: CachePlan, tim
     # K3 waits for a step's copies on the stream, so its events are compute alone),
     # else sampled timing and the arrival-gated K3 (engine.OffloadEngine.set_overlap)
     eng.set_copy_timing(1 if collect_cache_events else 8)
-    eng.set_overlap(not collect_cache_events)
+    from .engine import overlap_default
+    eng.set_overlap(not collect_cache_events and overlap_default())
     if strategy.kind == "eap" and not _eap_continue:
         eng.reset_eap()
     dev = torch.device("cuda", eng.device)
