@@ -430,6 +430,16 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (lg) lg->ondemand[i_od] = ce;
   }
   top -= n_od;
+  __syncwarp();
+  if (lane == 0) {
+    // the on-demand set is final: let the host start those copies now, before
+    // the drop list, the prediction and the K3 batch (system-scope release)
+    msg->n_od = n_od;
+    msg->od_bits = d.ondemand_bits;
+    msg->token = token;
+    msg->layer = layer;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&msg->seq_od), "r"((uint32_t)step + 1u) : "memory");
+  }
   const bool all_landed = __all_sync(FULL, !act || hit || (pref && arr));
   if (act) {
     C.prev_chosen[lane] = ce;
@@ -1565,7 +1575,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
   *g->copy_done_host = 0;
   *g->copy_done_host2 = 0;
-  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
+  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0, g->ring_host[i].seq_od = 0;
   const cudaStream_t cs = g->cstream;
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
   run_begin_kernel<<<1, 1, 0, cs>>>(g->d);
@@ -1573,6 +1583,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   FATE_CUDA(cudaStreamSynchronize(cs));
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] run_begin done\n");
   int launched = 0, processed = 0, k3_next = 0;
+  int od_sent = -1;  // last step whose on-demand copies went out at the early post
   const int lookahead = 4;
   const bool serial = serial_launches();
   // arrival-gated K3: launched right behind K1 (after the step's ARC update),
@@ -1691,6 +1702,16 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     }
     // service the step message of the next unprocessed step
     StepMsg &m = g->ring_host[processed % kRing];
+    // arrival-gated: the on-demand copies start as soon as K1 posts the set
+    // (they go ahead of every queued prefetch, as promote_ondemand orders them)
+    if (overlap && od_sent != processed && m.seq_od == (uint32_t)processed + 1u) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      for (int i = 0; i < m.n_od && status == FATE_OK; ++i)
+        status = ch.submit_one(Transfer{1, m.token, m.layer, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
+      if (status == FATE_OK) status = ch.flush_counters();
+      if (status) break;
+      od_sent = processed;
+    }
     if (m.seq == (uint32_t)processed + 1u) {
       std::atomic_thread_fence(std::memory_order_acquire);
       const double hm0 = hprof ? hnow() : 0.0;
@@ -1709,9 +1730,11 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       // prefetches for layer l+1 (issued at gate start, pipeline.py:414-417)
       for (int i = 0; i < m.n_pf; ++i)
         ch.pending.push_back(Transfer{0, t, l + 1, m.pf_e[i], m.pf_bits_each[i], m.pf_b[i], m.pf_g[i], -1, -1});
-      // on-demand loads for this step, promoted ahead of every prefetch
-      for (int i = 0; i < m.n_od; ++i)
-        ch.pending.push_back(Transfer{1, t, l, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
+      // on-demand loads for this step, promoted ahead of every prefetch (unless
+      // already submitted when the set was posted)
+      if (od_sent != processed)
+        for (int i = 0; i < m.n_od; ++i)
+          ch.pending.push_back(Transfer{1, t, l, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
       ch.promote();
       if (!m.self_signaled && !overlap) {
         // the compute stream may proceed once every needed transfer landed:
@@ -1740,7 +1763,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       if ((status = ch.pump())) break;
       if (hprof) h_msg += hnow() - hm0;
     }
-    if ((status = ch.pump())) break;
+    // (not between the two halves of a step's message: queued prefetches of this
+    // step may still be dropped)
+    if (od_sent != processed && (status = ch.pump())) break;
     if (m.seq != (uint32_t)processed + 1u) {
       _mm_pause();
       const cudaError_t qe = cudaStreamQuery(cs);
@@ -2427,7 +2452,7 @@ extern "C" int fate_engine_prefill(fate_engine *g, const double *gate_in_dev, co
   for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
   *g->copy_done_host = 0;
   *g->copy_done_host2 = 0;
-  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0;
+  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0, g->ring_host[i].seq_od = 0;
   EngineDev d = g->d;
   d.ready = g->ready_dev;
   prefill_begin_kernel<<<1, 1, 0, cs>>>(d);

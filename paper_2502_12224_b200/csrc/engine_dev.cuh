@@ -16,9 +16,11 @@ struct alignas(16) ArcLayer {
   int32_t t1[EMAX], t2[EMAX], b1[EMAX], b2[EMAX];
 };
 
-// Step message, device -> host (mapped pinned memory).  `seq` is written last.
+// Step message, device -> host (mapped pinned memory).  `seq` is written last;
+// `seq_od` earlier, as soon as the on-demand set (n_od, od_*) is final.
 struct StepMsg {
   volatile uint32_t seq;
+  volatile uint32_t seq_od;
   int32_t step, token, layer;
   int32_t self_signaled;
   int32_t n_od, n_need, n_drop, n_pf;
