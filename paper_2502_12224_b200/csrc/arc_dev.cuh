@@ -23,6 +23,12 @@ struct WarpArc {
     c = sm->c, n1 = sm->n1, n2 = sm->n2, nb1 = sm->nb1, nb2 = sm->nb2, p = sm->p;
   }
 
+  // lists already copied into shared memory (by the whole block)
+  __device__ void attach(ArcLayer *sm) {
+    s = sm;
+    c = sm->c, n1 = sm->n1, n2 = sm->n2, nb1 = sm->nb1, nb2 = sm->nb2, p = sm->p;
+  }
+
   __device__ void store(ArcLayer *g) {
     const int lane = threadIdx.x & 31;
     if (lane == 0) s->n1 = n1, s->n2 = n2, s->nb1 = nb1, s->nb2 = nb2, s->p = p;

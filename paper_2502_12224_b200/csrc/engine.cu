@@ -4,11 +4,12 @@
 //
 // Per decode step (token t, layer l) on the compute stream:
 //   K1  decode_gate_kernel   fp64 router rows of W_l and W_{l+1} (one CTA per
-//       row), then the last CTA: deferred ARC update of the previous step
-//       (cache.py:212-215), softmax/top-k of layer l, hit / prefetched /
-//       on-demand split (pipeline.py:441-459), cross-layer prediction for
-//       l+1 truncated to n and filtered by residency (pipeline.py:390-404),
-//       the K3 expert batch, and a step message to the host copy manager.
+//       row; each stores its logit into a slot the tail block polls), then the
+//       tail block: softmax/top-k of layer l, hit / prefetched / on-demand
+//       split (pipeline.py:441-459), cross-layer prediction for l+1 truncated
+//       to n and filtered by residency (pipeline.py:390-404), the K3 expert
+//       batch and a step message to the host copy manager (warp 0), and this
+//       step's ARC update_after_layer (cache.py:212-215, warp 1).
 //   WAIT cuStreamWaitValue32 on a host-mapped flag: set by K1 itself when
 //       every needed expert is already in HBM, otherwise by the host after
 //       the needed copies landed.
@@ -109,6 +110,13 @@ namespace {
 
 constexpr int kGateThreads = 256;
 
+// K1 row -> tail hand-off: every router-row slot holds this bit pattern (a
+// signalling NaN with a payload no arithmetic produces) until its row block
+// stores the logit; the tail polls the slots themselves (an aligned 8-byte
+// store is single-copy atomic), so the value is its own ready flag -- no
+// fence, arrive counter or second read -- and re-arms them once consumed.
+constexpr unsigned long long kLogitEmpty = 0xFFF4DEADBEEF0001ull;
+
 __device__ __forceinline__ int pop_free(const EngineDev &d) {
   Ctrl &C = *d.ctrl;
   if (C.free_top <= 0) {
@@ -172,13 +180,67 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
   __syncwarp();
 }
 
+// update_after_layer of the step K1 is deciding (cache.py:212-215), by warp 1
+// of K1's tail block once warp 0 has made every free-stack edit of the step:
+// ARC accesses in ascending id order over the layer's lists (copied into
+// shared memory while the router rows ran), buffer hand-over as in
+// apply_prev_update, every input from shared memory (chosen ids, their
+// buffers, the layer's buffer table, the free-stack top).
+__device__ void apply_step_update(const EngineDev &d, ArcLayer *arc_sm, const int32_t *chosen, const int32_t *cbuf,
+                                  int32_t *bof, int k, int layer, int top, fate_step_log *lg, int32_t *rel) {
+  const int lane = threadIdx.x & 31;
+  WarpArc arc;
+  arc.attach(arc_sm);
+  int nrel = 0, nvic = 0;
+  for (int i = 0; i < k; ++i) {
+    const int e = chosen[i];
+    int victim;
+    const int hit = arc.access(e, &victim);
+    if (lane == 0) {
+      if (victim >= 0) {
+        const int slot = bof[victim];
+        if (slot >= 0) rel[nrel++] = slot;
+        bof[victim] = -1;
+        d.buf_of[layer * d.E + victim] = -1;
+        if (lg && nvic < KMAX) lg->victims[nvic] = victim;
+        ++nvic;
+      }
+      if (!hit) {
+        const int b = cbuf[i];
+        if (arc.c >= 1) {
+          bof[e] = b;
+          d.buf_of[layer * d.E + e] = b;
+          for (int r = 0; r < nrel; ++r)
+            if (rel[r] == b) rel[r] = rel[--nrel], r = nrel;
+        } else {
+          rel[nrel++] = b;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  arc.store(&d.arc[layer]);
+  if (lane == 0) {
+    Ctrl &C = *d.ctrl;
+    for (int r = 0; r < nrel; ++r) {
+      if (top >= d.nbuf) {
+        C.err = 2;
+        break;
+      }
+      d.free_stack[top++] = rel[r];
+    }
+    C.free_top = top;
+    if (lg) lg->n_victims = nvic;
+  }
+}
+
 // K1 phase timestamps of the last launch (globaltimer ns), diagnostics only:
 // [0] block 0 start, [1] tail start, [2] state staged, [3] routed, [4] split,
 // [5] predicted, [6] message posted
 __device__ unsigned long long g_k1_prof[16];
 // FATE_PROF accumulators over a run: [0] sum(K3 end -> K1 block 0 start), [1] n,
 // [2] sum(K1 block 0 start -> message posted), [3] n
-__device__ unsigned long long g_k1_acc[4];
+__device__ unsigned long long g_k1_acc[8];
 __device__ unsigned long long g_k1_t0;
 #ifdef FATE_PROF
 #define K1_STAMP(i) (g_k1_prof[i] = gtime1())
@@ -197,6 +259,10 @@ struct TailSmem {
   uint32_t pgen_l[EMAX], pdone_l[EMAX];
   int32_t pred_prev[EMAX];
   int32_t c_free_top, c_step, c_pred_valid, c_pred_layer, c_pred_n, shared_present;
+  const uint8_t *shared_ptr;
+  float shared_w;
+  int32_t od_buf[KMAX];
+  uint32_t od_gen[KMAX];
   int32_t eap_prev[KMAX], eap_prev_ok;
   double z[2 * EMAX], w[2 * EMAX];
   int32_t ord[2 * EMAX];
@@ -211,20 +277,24 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
                                                                    volatile uint32_t *ready_host, int token) {
   __shared__ double red[kGateThreads / 32];
   __shared__ TailSmem S;
+  __shared__ ArcLayer arc_sm;
+  __shared__ int32_t arc_rel[4 * KMAX + 4];
   __shared__ int32_t tchosen[KMAX];
   const int E = d.E, H = d.H, L = d.L;
   const double *h = gate_in + ((int64_t)token * L + layer) * H;
   // block 0: the tail (stages state while the others work); blocks
   // 1..n_rows: router rows; last block: the FFN input x and its K3 layouts.
-  // The previous step's deferred update_after_layer ran in arc_update_kernel
-  // on the side stream (overlapping that step's transfers and K3) and
-  // completed before this launch.
+  // The previous step's update_after_layer ran in the previous K1 (warp 1 of
+  // its tail block) and completed before this launch.
   const int n_rows = gridDim.x - 2;
   const int row = blockIdx.x - 1;
   if (blockIdx.x == gridDim.x - 1) {
     // FFN input x = sqrt(H) * gate_in (fp64 product, fp32 storage) -> K3 layouts
     const double sH = sqrt((double)H);
     for (int i = threadIdx.x; i < H; i += kGateThreads) S.xs[i] = (float)(sH * h[i]);
+    // launched programmatically behind the previous step's K3: that K3 reads x
+    // until it completes (no-op for a normal launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     write_xlay(S.xs, H, reinterpret_cast<float4 *>(d.x), threadIdx.x, kGateThreads);
     return;
@@ -233,7 +303,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     K1_STAMP(0);
 #ifdef FATE_PROF
     // previous K3's end -> this launch (both globaltimer)
-    const unsigned long long e = d.stats->ffn.end_ns, now = gtime1();
+    const unsigned long long e = d.stats->ffn.end_max_ns, now = gtime1();
     if (e && now > e) g_k1_acc[0] += now - e, g_k1_acc[1] += 1;
     g_k1_t0 = now;
 #endif
@@ -274,14 +344,9 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (threadIdx.x == 0) {
       double sum = 0.0;
       for (int w = 0; w < kGateThreads / 32; ++w) sum += red[w];
-      d.logits[row] = __ddiv_rn(sum, tau);
-    }
-  }
-  if (blockIdx.x > 0) {
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned prev = atomicAdd(&d.ctrl->arrive, 1u);
-      if (prev == (unsigned)n_rows - 1u) K1_STAMP(11);  // last arrival
+      const double z = __ddiv_rn(sum, tau);
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(d.logits + row), "l"(__double_as_longlong(z))
+                   : "memory");
     }
     return;
   }
@@ -304,24 +369,48 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   }
   if (threadIdx.x < d.k && trace_chosen) tchosen[threadIdx.x] = trace_chosen[((int64_t)token * L + layer) * d.k + threadIdx.x];
   if (threadIdx.x < KMAX) S.eap_prev[threadIdx.x] = threadIdx.x < C.prev_k ? C.prev_chosen[threadIdx.x] : 0;
+  // the control block was last written by the previous K1 / ARC update, both
+  // complete before this launch (stream order): stage it with the tables
+  const int c_pred_n = C.pred_n;
+  const int c_top = C.free_top;
+  if (threadIdx.x < KMAX) {
+    // on-demand pops come off the top of the free stack (at most k): their
+    // buffers and generations, so the split does no dependent global loads
+    const int i = c_top - 1 - (int)threadIdx.x;
+    const int b = i >= 0 && i < d.nbuf ? d.free_stack[i] : 0;
+    S.od_buf[threadIdx.x] = b;
+    S.od_gen[threadIdx.x] = d.buf_gen[b];
+  }
+  for (int i = threadIdx.x; i < c_pred_n; i += kGateThreads) S.pred_prev[i] = C.pred_list[i];
+  // this layer's ARC lists for warp 1's update (written last by this layer's
+  // previous update, in an earlier launch)
+  for (int i = threadIdx.x; i < (int)(sizeof(ArcLayer) / 16); i += kGateThreads)
+    reinterpret_cast<int4 *>(&arc_sm)[i] = reinterpret_cast<const int4 *>(&d.arc[layer])[i];
   if (threadIdx.x == 0) {
     S.c_step = C.step;
     S.c_pred_valid = C.pred_valid;
     S.c_pred_layer = C.pred_layer;
-    S.c_pred_n = C.pred_n;
+    S.c_pred_n = c_pred_n;
+    S.c_free_top = c_top;
     // EAP observe needs the chosen set of (token, layer - 1): the previous step
     // (prev_valid is cleared once the deferred ARC update ran; the chosen set stays)
     S.eap_prev_ok = layer > 0 && C.step > 0 && C.prev_layer == layer - 1 ? 1 : 0;
-    S.shared_present = d.shared && d.shared[layer] ? 1 : 0;
-    // wait for the router rows and the ARC block
-    while (*(volatile uint32_t *)&C.arrive < (uint32_t)n_rows) {
-    }
-    __threadfence();
-    K1_STAMP(1);
-    S.c_free_top = *(volatile int32_t *)&C.free_top;
+    const uint8_t *sh = d.shared ? d.shared[layer] : nullptr;
+    S.shared_ptr = sh;
+    S.shared_present = sh ? 1 : 0;
+    S.shared_w = sh && d.shared_gate ? d.shared_gate[layer] : 1.0f;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n_rows; i += kGateThreads) S.z[i] = ((volatile double *)d.logits)[i];
+  // the router rows: poll each slot until its row block stored the logit,
+  // then re-arm it for the next launch
+  for (int i = threadIdx.x; i < n_rows; i += kGateThreads) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(d.logits + i) : "memory");
+    } while (v == kLogitEmpty);
+    S.z[i] = __longlong_as_double((long long)v);
+    reinterpret_cast<unsigned long long *>(d.logits)[i] = kLogitEmpty;
+  }
+  if (threadIdx.x == 0) K1_STAMP(1);
   for (int i = threadIdx.x; i < E; i += kGateThreads) {
     if (pl == layer) {
       const int bb = ((volatile int32_t *)d.buf_of)[layer * E + i];
@@ -331,7 +420,6 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     if (pl == layer + 1 && layer + 1 < L) S.bof_n[i] = ((volatile int32_t *)d.buf_of)[(layer + 1) * E + i];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < S.c_pred_n; i += kGateThreads) S.pred_prev[i] = C.pred_list[i];
   // (2) routing of layer l and the cross-layer prediction for l+1: the two
   // softmaxes on warps 0 and 1 at once, then the ranks by the whole block
   const bool pred_seg = d.use_predictor && d.policy != 2 && layer + 1 < L;
@@ -341,9 +429,28 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (threadIdx.x < kGateThreads / 2) rank_by_weight(S.w, S.ord, E, threadIdx.x, kGateThreads / 2);
   else if (pred_seg) rank_by_weight(S.w + E, S.ord + E, E, threadIdx.x - kGateThreads / 2, kGateThreads / 2);
   __syncthreads();
-  if (threadIdx.x >= 32) return;
+  if (threadIdx.x >= 64) return;
+  if (threadIdx.x >= 32) {
+    // warp 1: update_after_layer of this step (cache.py:212-215) once warp 0
+    // has finished every free-stack edit of the step (named barrier 1), in
+    // parallel with the K3 batch and the step message
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+#ifdef FATE_PROF
+    const unsigned long long ta = gtime1();
+#endif
+    apply_step_update(d, &arc_sm, S.chosen, S.cbuf, S.bof_l, d.k, layer, S.c_free_top, log ? log + S.c_step : nullptr,
+                      arc_rel);
+#ifdef FATE_PROF
+    if (threadIdx.x == 32) {
+      const unsigned long long tb = gtime1();
+      g_k1_acc[4] += ta - g_k1_t0;
+      g_k1_acc[5] += tb - g_k1_t0;
+      g_k1_acc[6] += 1;
+    }
+#endif
+    return;
+  }
   const int lane = threadIdx.x;
-  if (lane == 0) C.arrive = 0;
   const int k = d.k;
   const int step = S.c_step;
   fate_step_log *lg = log ? log + step : nullptr;
@@ -395,6 +502,9 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     }
   }
   if (lane == 0) K1_STAMP(3);
+  // the previous step's K3 has completed (programmatic launch): it no longer
+  // reads the buffers popped below, the batch or x (no-op for a normal launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // (3) hit / prefetched / on-demand split (pipeline.py:441-459), one lane per chosen expert
   StepMsg *msg = d.ring + (step % kRing);
   int top = S.c_free_top;
@@ -417,9 +527,9 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     msg->need_b[i_need] = b;
   }
   if (odm) {
-    // pop n_od buffers off the free stack: the first od takes the top
-    b = d.free_stack[top - 1 - i_od];
-    const uint32_t g = d.buf_gen[b] + 1u;
+    // pop n_od buffers off the free stack: the first od takes the top (staged)
+    b = S.od_buf[i_od];
+    const uint32_t g = S.od_gen[i_od] + 1u;
     d.buf_gen[b] = g;
     want = g;
     src = d.ondemand_bits;
@@ -431,9 +541,10 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   }
   top -= n_od;
   __syncwarp();
-  if (lane == 0) {
+  if (lane == 0 && n_od) {
     // the on-demand set is final: let the host start those copies now, before
-    // the drop list, the prediction and the K3 batch (system-scope release)
+    // the drop list, the prediction and the K3 batch (system-scope release;
+    // with nothing to load the full message below carries the step)
     msg->n_od = n_od;
     msg->od_bits = d.ondemand_bits;
     msg->token = token;
@@ -544,6 +655,10 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (lane == 0) {
     if (top < 0 || top > d.nbuf) C.err = 1;
     C.free_top = top;
+    S.c_free_top = top;  // warp 1 pushes the step's released buffers from here
+    C.prev_layer = layer;  // (EAP observe of the next step reads the chosen set)
+    C.prev_k = k;
+    C.prev_step = step;
     if (n_pred >= 0) {
       C.pred_n = n_pred;
       C.pred_layer = layer + 1;
@@ -557,6 +672,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     atomicAdd(&d.stats->ondemand_issued, (unsigned long long)n_od);
     atomicAdd(&d.stats->prefetch_issued, (unsigned long long)n_pf);
   }
+  __syncwarp();
+  asm volatile("bar.arrive 1, 64;" ::: "memory");  // hand the ARC update to warp 1
   if (lane == 0) K1_STAMP(5);
   // (6) the K3 batch: routed experts weighted by their full-softmax routing
   // weight (not renormalised), plus the shared expert with weight 1.
@@ -569,8 +686,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   if (lane == 0) {
     int n = k, off = k * d.I;
     if (S.shared_present) {
-      B.e[n] = FfnExpert{d.shared[layer], d.shared_gate ? d.shared_gate[layer] : 1.0f, d.I_shared, d.shared_bits, 0,
-                         -1, 0u};
+      B.e[n] = FfnExpert{S.shared_ptr, S.shared_w, d.I_shared, d.shared_bits, 0, -1, 0u};
       off += d.I_shared;
       ++n;
     }
@@ -597,10 +713,6 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     // system scope (the host polls the mapped ring)
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&msg->seq), "r"((uint32_t)step + 1u) : "memory");
     // (9) control block for the next step
-    C.prev_valid = 1;
-    C.prev_layer = layer;
-    C.prev_k = k;
-    C.prev_step = step;
     C.cur_token = token;
     C.cur_layer = layer;
     C.step = step + 1;
@@ -608,8 +720,10 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     K1_STAMP(6);
     K1_STAMP(7);
 #ifdef FATE_PROF
-    g_k1_acc[2] += gtime1() - g_k1_t0;
+    const unsigned long long tp = gtime1();
+    g_k1_acc[2] += tp - g_k1_t0;
     g_k1_acc[3] += 1;
+    d.stats->ffn.k1_post_ns = tp;
 #endif
   }
 }
@@ -698,6 +812,7 @@ __global__ void engine_reset_kernel(EngineDev d, const int32_t *caps) {
     d.buf_gen[i] = 0;
     d.buf_done[i] = 0xFFFFFFFFu;
   }
+  for (int i = tid; i < 2 * EMAX; i += nth) reinterpret_cast<unsigned long long *>(d.logits)[i] = kLogitEmpty;
   for (int l = tid; l < d.L; l += nth) {
     ArcLayer &a = d.arc[l];
     a.c = caps[l];
@@ -725,6 +840,7 @@ __global__ void run_begin_kernel(EngineDev d) {
     C.prev_valid = 0;
     C.pred_valid = 0;
     C.err = 0;
+    for (int i = 0; i < 2 * EMAX; ++i) reinterpret_cast<unsigned long long *>(d.logits)[i] = kLogitEmpty;
     // pending prefetches never outlive a run
     for (int i = 0; i < d.L * d.E; ++i) {
       if (d.pend_buf[i] >= 0) push_free(d, d.pend_buf[i]);
@@ -1585,6 +1701,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   int launched = 0, processed = 0, k3_next = 0;
   int od_sent = -1;  // last step whose on-demand copies went out at the early post
   const int lookahead = 4;
+  const bool k1_pdl = getenv("FATE_K1_NOPDL") == nullptr;  // experiment toggle
   const bool serial = serial_launches();
   // arrival-gated K3: launched right behind K1 (after the step's ARC update),
   // each expert's pieces start once its copy landed, so K3 works through the
@@ -1659,10 +1776,10 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     while (launched < n_steps && launched < processed + (serial ? 1 : lookahead) && (!serial || k3_next == launched)) {
       const int s = launched, t = s / L, l = s % L;
       const double hf0 = hprof ? hnow() : 0.0;
-      // tail block + router rows of W_l (and W_{l+1} when predicting) + the deferred-ARC block
-      // tail block + router rows of W_l (and W_{l+1} when predicting)
+      // tail block + router rows of W_l (and W_{l+1} when predicting) + the x block
       const int rows = ((rows_pred == 2 && l + 1 < L) ? 2 * g->cfg.num_experts : g->cfg.num_experts) + 2;
-      FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));  // previous step's ARC update applied
+      // any ARC update the side stream still runs (cache protocol calls before the run)
+      if (s == 0) FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));
       if (g->dense) {
         // the dense part of (t, l): attention block + shared-expert gate (dense.cu)
         if (ksamp(s)) FATE_CUDA(cudaEventRecord(dev_[2 * s], cs));
@@ -1673,22 +1790,31 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         if (ksamp(s)) FATE_CUDA(cudaEventRecord(dev_[2 * s + 1], cs));
       }
       if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s], cs));
-      decode_gate_kernel<<<rows, kGateThreads, 0, cs>>>(g->d, gate_in_dev, chosen_dev, log_dev, l,
-                                                        (volatile uint32_t *)g->ready_dev, t);
+      {
+        // programmatic launch behind the previous K3 (its launch processing and
+        // the router rows overlap K3's last CTAs; the tail and x blocks wait
+        // for K3's completion before touching anything K3 reads).  Not with the
+        // dense part, whose kernels produce K1's inputs.
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(rows);
+        lc.blockDim = dim3(kGateThreads);
+        lc.stream = cs;
+        cudaLaunchAttribute la[1];
+        la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        la[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = la;
+        lc.numAttrs = (k1_pdl && !g->dense && !serial && s > 0) ? 1 : 0;
+        FATE_CUDA(cudaLaunchKernelEx(&lc, decode_gate_kernel, g->d, (const double *)gate_in_dev,
+                                     (const int32_t *)chosen_dev, log_dev, l, (volatile uint32_t *)g->ready_dev, t));
+      }
       FATE_CHECK_LAUNCH("decode_gate_kernel");
       if (ksamp(s)) FATE_CUDA(cudaEventRecord(kev[4 * s + 1], cs));
-      // update_after_layer of this step (pipeline.py:483) on the side stream
-      FATE_CUDA(cudaEventRecord(g->ev_k1, cs));
-      FATE_CUDA(cudaStreamWaitEvent(g->astream, g->ev_k1, 0));
-      arc_update_kernel<<<1, 32, 0, g->astream>>>(g->d, log_dev);
-      FATE_CHECK_LAUNCH("arc_update_kernel (step update)");
-      FATE_CUDA(cudaEventRecord(g->ev_arc, g->astream));
+      // update_after_layer of this step (pipeline.py:483) runs inside K1 (warp 1
+      // of the tail block), so K3 follows K1 directly on this stream
       if (dbg && s < 2) fprintf(stderr, "[fate] launched K1 step %d\n", s);
       // serial mode: no stream wait at all (the host enqueues K3 only once the flag is set);
-      // arrival-gated: K3 itself waits per expert, behind this step's ARC update
-      // (K3 holds every SM while it waits, the update must not queue behind it)
-      if (overlap) FATE_CUDA(cudaStreamWaitEvent(cs, g->ev_arc, 0));
-      else if (!serial)
+      // arrival-gated: K3 itself waits per expert
+      if (!overlap && !serial)
         FATE_CU(p_wait32((CUstream)cs, (CUdeviceptr)(g->ready_dev + l), (uint32_t)t + 1u, CU_STREAM_WAIT_VALUE_GEQ));
       if (dbg && s < 2) fprintf(stderr, "[fate] enqueued wait step %d\n", s);
       if (!serial && (status = ffn_step(s))) break;
@@ -1793,16 +1919,21 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     cudaStreamSynchronize(cs);
     DevStats dsp{};
     cudaMemcpy(&dsp, g->d.stats, sizeof(dsp), cudaMemcpyDeviceToHost);
-    unsigned long long acc[4] = {0, 0, 0, 0};
+    unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #ifdef FATE_PROF
     cudaMemcpyFromSymbol(acc, g_k1_acc, sizeof(acc));
-    const unsigned long long z[4] = {0, 0, 0, 0};
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_k1_acc, z, sizeof(z));
+    if (acc[6])
+      fprintf(stderr, "[fate] K1 warp-1 ARC update from K1 block start: begins %.2f us, ends %.2f us\n",
+              acc[4] * 1e-3 / acc[6], acc[5] * 1e-3 / acc[6]);
 #endif
     fprintf(stderr, "[fate] device us/step: K3 tail after its last gate opened %.2f (%llu launches waited); "
-            "K3 end -> K1 block start %.2f; K1 block start -> message posted %.2f (profiling builds)\n",
+            "K3 last CTA end -> K1 block start %.2f; K1 block start -> message posted %.2f; "
+            "K1 posted -> K3 CTA 0 start %.2f (profiling builds)\n",
             dsp.ffn.tail_n ? dsp.ffn.tail_ns * 1e-3 / dsp.ffn.tail_n : 0.0, dsp.ffn.tail_n,
-            acc[1] ? acc[0] * 1e-3 / acc[1] : 0.0, acc[3] ? acc[2] * 1e-3 / acc[3] : 0.0);
+            acc[1] ? acc[0] * 1e-3 / acc[1] : 0.0, acc[3] ? acc[2] * 1e-3 / acc[3] : 0.0,
+            dsp.ffn.k1k3_n ? dsp.ffn.k1k3_ns * 1e-3 / dsp.ffn.k1k3_n : 0.0);
   }
   if (getenv("FATE_DEBUG"))
     fprintf(stderr, "[fate] decode loop exit status=%d processed=%d/%d pending=%zu inflight=%zu err=%s\n", status,

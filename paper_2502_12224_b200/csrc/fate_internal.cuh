@@ -139,6 +139,9 @@ struct FfnStats {
   // summed time from it to the launch's end (the K3 work left after the last
   // copy landed) and how many launches waited; the last launch's end
   unsigned long long open_max, tail_ns, tail_n, end_ns;
+  // profiling builds: the last CTA's end (max over CTAs), K1's message-posted
+  // time, and the summed K1 posted -> K3 CTA start hand-off
+  unsigned long long end_max_ns, k1_post_ns, k1k3_ns, k1k3_n;
 };
 
 // landed (device memory, per staging buffer) / abort (host-mapped; 0x7FFFFFFF

@@ -674,6 +674,13 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (lane == 0) K3_PROF(0);
+#ifdef FATE_PROF
+    if (blockIdx.x == 0 && lane == 0 && stat && stat->k1_post_ns) {
+      const unsigned long long t = gclock();
+      if (t > stat->k1_post_ns) stat->k1k3_ns += t - stat->k1_post_ns, stat->k1k3_n += 1;
+      stat->k1_post_ns = 0;
+    }
+#endif
     make_plan(batch, plan, G, blockIdx.x, lane);
     if (lane == 0) K3_PROF(1);
   }
@@ -907,6 +914,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
     }
   }
   if (ctid == 0) K3_PROF(6);
+#ifdef FATE_PROF
+  if (ctid == 0 && stat) atomicMax(&stat->end_max_ns, gclock());
+#endif
   if (blockIdx.x == 0 && ctid == 0 && stat) {
     // CTA 0's rows are its last work; the other CTAs finish theirs within ~1 us
     const unsigned long long t = gclock(), o = *(volatile unsigned long long *)&stat->open_max;
@@ -1017,7 +1027,7 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = getenv("FATE_K3_NONCOOP") ? 0 : 1;  // experiment toggle
   if (H == 2048) return cudaLaunchKernelEx(&cfg, ffn_kernel<2048>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
   if (H == 4096) return cudaLaunchKernelEx(&cfg, ffn_kernel<4096>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
   return cudaLaunchKernelEx(&cfg, ffn_kernel<0>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
