@@ -254,6 +254,11 @@ __device__ __forceinline__ unsigned long long gtime1() {
   return t;
 }
 
+// relaxed system-scope 8-byte store (single-copy atomic) into the mapped ring
+__device__ __forceinline__ void st_sys64(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 struct TailSmem {
   int32_t bof_l[EMAX], pend_l[EMAX], bof_n[EMAX], bbits_l[EMAX];
   uint32_t pgen_l[EMAX], pdone_l[EMAX];
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
   // reads the buffers popped below, the batch or x (no-op for a normal launch)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // (3) hit / prefetched / on-demand split (pipeline.py:441-459), one lane per chosen expert
-  StepMsg *msg = d.ring + (step % kRing);
+  DecodeMsg *msg = d.dring + (step % kRing);
   int top = S.c_free_top;
   const int slot_b = act ? S.bof_l[ce] : -1;
   const int pend_b = act && slot_b < 0 ? S.pend_l[ce] : -1;
@@ -523,8 +528,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     src = d.prefetch_bits;
     arr = S.pdone_l[ce] == S.pgen_l[ce];
     want = S.pgen_l[ce];
-    msg->need_e[i_need] = ce;
-    msg->need_b[i_need] = b;
+    st_sys64(&msg->need[i_need], msg_entry(step, ce, b, 0u));
   }
   if (odm) {
     // pop n_od buffers off the free stack: the first od takes the top (staged)
@@ -534,22 +538,16 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     want = g;
     src = d.ondemand_bits;
     d.buf_bits[b] = d.ondemand_bits;
-    msg->od_e[i_od] = ce;
-    msg->od_b[i_od] = b;
-    msg->od_g[i_od] = g;
+    st_sys64(&msg->od[i_od], msg_entry(step, ce, b, g));
     if (lg) lg->ondemand[i_od] = ce;
   }
   top -= n_od;
-  __syncwarp();
   if (lane == 0 && n_od) {
     // the on-demand set is final: let the host start those copies now, before
-    // the drop list, the prediction and the K3 batch (system-scope release;
-    // with nothing to load the full message below carries the step)
-    msg->n_od = n_od;
-    msg->od_bits = d.ondemand_bits;
-    msg->token = token;
-    msg->layer = layer;
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&msg->seq_od), "r"((uint32_t)step + 1u) : "memory");
+    // the drop list, the prediction and the K3 batch (with nothing to load the
+    // full message below carries the step)
+    st_sys64(&msg->od_head, ((uint64_t)((uint32_t)step + 1u) << 32) | ((uint64_t)n_od << 23) |
+                                ((uint64_t)(d.ondemand_bits & 31) << 18));
   }
   const bool all_landed = __all_sync(FULL, !act || hit || (pref && arr));
   if (act) {
@@ -578,8 +576,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     const unsigned m = __ballot_sync(FULL, drop);
     if (drop) {
       const int i = n_drop + __popc(m & lt);
-      msg->drop_e[i] = e;
-      msg->drop_b[i] = pb;
+      st_sys64(&msg->drop[i], msg_entry(step, e, pb, 0u));
       d.free_stack[top + __popc(m & lt)] = pb;
     }
     top += __popc(m);
@@ -641,10 +638,7 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
         d.buf_bits[nb] = d.prefetch_bits;
         d.pend_buf[(layer + 1) * E + e] = nb;
         d.pend_gen[(layer + 1) * E + e] = g;
-        msg->pf_e[j] = e;
-        msg->pf_b[j] = nb;
-        msg->pf_g[j] = g;
-        msg->pf_bits_each[j] = d.prefetch_bits;
+        st_sys64(&msg->pf[j], msg_entry(step, e, nb, g));
         if (lg) lg->prefetch[j] = e;
       }
       top -= __popc(m);
@@ -694,24 +688,11 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     B.n = n;
     B.total_I = off;
     B.work = 0u;
-    // (7) step message + (8) self-signal when nothing must be waited for
-    msg->n_od = n_od;
-    msg->n_need = n_need;
-    msg->n_drop = n_drop;
-    msg->n_pf = n_pf;
-    msg->od_bits = d.ondemand_bits;
-    msg->pf_bits = d.prefetch_bits;
-    msg->step = step;
-    msg->token = token;
-    msg->layer = layer;
-    msg->self_signaled = all_landed ? 1 : 0;
+    // (7) self-signal when nothing must be waited for + (8) the step message
+    // head (the entries carry their own tags: no fence)
     if (all_landed) ready_host[layer] = (uint32_t)token + 1u;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    // publish: every lane's message fields (ordered by __syncwarp) before seq,
-    // system scope (the host polls the mapped ring)
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(&msg->seq), "r"((uint32_t)step + 1u) : "memory");
+    st_sys64(&msg->head, ((uint64_t)msg_head_tag(step) << 33) | ((uint64_t)n_need << 24) | ((uint64_t)n_drop << 15) |
+                             ((uint64_t)n_pf << 6) | ((uint64_t)(d.prefetch_bits & 31) << 1) | (all_landed ? 1u : 0u));
     // (9) control block for the next step
     C.cur_token = token;
     C.cur_layer = layer;
@@ -887,6 +868,7 @@ struct fate_engine {
   void *k3_scratch = nullptr;  // K3 per-CTA partials + grid-barrier word (this engine's launches only)
   // mapped pinned host memory
   StepMsg *ring_host = nullptr;
+  DecodeMsg *dring_host = nullptr;
   volatile uint32_t *ready_host = nullptr;     // [L]
   uint32_t *ready_dev = nullptr;
   size_t eap_bytes = 0;  // eap_counts .. end of eap_totals (contiguous in dev_block)
@@ -1018,6 +1000,11 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   const int staging_decode = 2 * n_max + 2 * k + 4;
   const int staging_prefill = 2 * E + 4;
   const int nbuf = S + std::max(staging_decode, staging_prefill);
+  if (nbuf > 0xFFFF) {
+    set_error("fate_engine_create: more than 65535 expert buffers (the decode message packs buffer ids in 16 bits)");
+    delete g;
+    return FATE_EINVAL;
+  }
   int64_t bb = 0;
   for (int b : {cfg->prefetch_bits, cfg->ondemand_bits, cfg->cached_bits, cfg->prefill_ondemand_bits, 4, 2})
     bb = std::max<int64_t>(bb, buffer_bytes(H, I, b));
@@ -1094,6 +1081,11 @@ extern "C" int fate_engine_create(const fate_engine_config *cfg, fate_engine **o
   void *pd = nullptr;
   FATE_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
   d.ring = (StepMsg *)pd;
+  FATE_CUDA(cudaHostAlloc(&p, sizeof(DecodeMsg) * kRing, cudaHostAllocMapped));
+  memset(p, 0, sizeof(DecodeMsg) * kRing);
+  g->dring_host = (DecodeMsg *)p;
+  FATE_CUDA(cudaHostGetDevicePointer(&pd, p, 0));
+  d.dring = (DecodeMsg *)pd;
   FATE_CUDA(cudaHostAlloc(&p, 4096, cudaHostAllocMapped));
   memset(p, 0, 4096);
   g->ready_host = (volatile uint32_t *)p;
@@ -1160,6 +1152,7 @@ extern "C" int fate_engine_destroy(fate_engine *g) {
   if (g->pf_block) cudaFree(g->pf_block);
   if (g->dense_block) cudaFree(g->dense_block);
   cudaFreeHost(g->ring_host);
+  cudaFreeHost(g->dring_host);
   cudaFreeHost((void *)g->ready_host);
   delete g;
   return FATE_OK;
@@ -1635,6 +1628,28 @@ struct Channel {
 
 }  // namespace
 
+// one tagged word of a decode step message (engine_dev.cuh: DecodeMsg): K1
+// stored it before the head the host already saw, so it is at most a few
+// PCIe writes away
+static int msg_word(const uint64_t *p, int step, uint64_t *out) {
+  const uint32_t tag = msg_entry_tag(step);
+  for (long spin = 0;; ++spin) {
+    const uint64_t w = *(const volatile uint64_t *)p;
+    if ((uint32_t)(w >> 56) == tag) {
+      *out = w;
+      return FATE_OK;
+    }
+    if (spin > (1l << 28)) {
+      set_error("fate_engine_decode: a step-message entry never arrived");
+      return FATE_ETIMEOUT;
+    }
+    _mm_pause();
+  }
+}
+static inline int msg_e(uint64_t w) { return (int)((w >> 48) & 0xFF); }
+static inline int msg_b(uint64_t w) { return (int)((w >> 32) & 0xFFFF); }
+static inline uint32_t msg_g(uint64_t w) { return (uint32_t)w; }
+
 extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, const int32_t *chosen_dev, int T,
                                   float *y_dev, fate_step_log *log_dev, fate_run_stats *stats) {
   std::lock_guard<std::mutex> lock(g->mu);
@@ -1691,7 +1706,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   for (int l = 0; l < L; ++l) g->ready_host[l] = 0;
   *g->copy_done_host = 0;
   *g->copy_done_host2 = 0;
-  for (int i = 0; i < kRing; ++i) g->ring_host[i].seq = 0, g->ring_host[i].seq_od = 0;
+  memset(g->dring_host, 0, sizeof(DecodeMsg) * kRing);  // tags of an earlier run never match
   const cudaStream_t cs = g->cstream;
   if (getenv("FATE_DEBUG")) fprintf(stderr, "[fate] decode begin T=%d steps=%d\n", T, n_steps);
   run_begin_kernel<<<1, 1, 0, cs>>>(g->d);
@@ -1748,7 +1763,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       last_beat = std::chrono::steady_clock::now();
       fprintf(stderr, "[fate] beat processed=%d launched=%d pending=%zu inflight=%zu submitted=%u copy_done=%u seq=%u\n",
               processed, launched, ch.pending.size(), ch.inflight.size(), ch.submitted, *g->copy_done_host,
-              g->ring_host[processed % kRing].seq);
+              (unsigned)(g->dring_host[processed % kRing].head >> 33));
     }
     // profiling mode (FATE_PROFILE_SERIAL, e.g. under ncu, which serializes
     // launches): K3 of a step is enqueued only after the host has serviced that
@@ -1827,24 +1842,37 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       }
     }
     // service the step message of the next unprocessed step
-    StepMsg &m = g->ring_host[processed % kRing];
+    DecodeMsg &m = g->dring_host[processed % kRing];
+    const uint64_t head = *(volatile uint64_t *)&m.head;
+    const bool head_ok = (uint32_t)(head >> 33) == msg_head_tag(processed);
     // arrival-gated: the on-demand copies start as soon as K1 posts the set
     // (they go ahead of every queued prefetch, as promote_ondemand orders them)
-    if (overlap && od_sent != processed && m.seq_od == (uint32_t)processed + 1u) {
-      std::atomic_thread_fence(std::memory_order_acquire);
-      for (int i = 0; i < m.n_od && status == FATE_OK; ++i)
-        status = ch.submit_one(Transfer{1, m.token, m.layer, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
-      if (status == FATE_OK) status = ch.flush_counters();
-      if (status) break;
-      od_sent = processed;
+    if (overlap && od_sent != processed && !head_ok) {
+      const uint64_t oh = *(volatile uint64_t *)&m.od_head;
+      if ((uint32_t)(oh >> 32) == (uint32_t)processed + 1u) {
+        const int t = processed / L, l = processed % L;
+        const int n_od = (int)((oh >> 23) & 0x1FF), od_bits = (int)((oh >> 18) & 31);
+        for (int i = 0; i < n_od && status == FATE_OK; ++i) {
+          uint64_t w;
+          if ((status = msg_word(&m.od[i], processed, &w))) break;
+          status = ch.submit_one(Transfer{1, t, l, msg_e(w), od_bits, msg_b(w), msg_g(w), -1, -1});
+        }
+        if (status == FATE_OK) status = ch.flush_counters();
+        if (status) break;
+        od_sent = processed;
+      }
     }
-    if (m.seq == (uint32_t)processed + 1u) {
-      std::atomic_thread_fence(std::memory_order_acquire);
+    if (head_ok) {
       const double hm0 = hprof ? hnow() : 0.0;
-      const int t = m.token, l = m.layer;
+      const int t = processed / L, l = processed % L;
+      const int n_need = (int)((head >> 24) & 0x1FF), n_drop = (int)((head >> 15) & 0x1FF);
+      const int n_pf = (int)((head >> 6) & 0x1FF), pf_bits = (int)((head >> 1) & 31);
+      const bool self_signaled = head & 1u;
+      uint64_t w;
       // drop queued prefetches for this step that the gate did not choose
-      for (int i = 0; i < m.n_drop; ++i) {
-        const int e = m.drop_e[i];
+      for (int i = 0; i < n_drop && status == FATE_OK; ++i) {
+        if ((status = msg_word(&m.drop[i], processed, &w))) break;
+        const int e = msg_e(w);
         auto it = std::find_if(ch.pending.begin(), ch.pending.end(), [&](const Transfer &x) {
           return x.kind == 0 && x.layer == l && x.expert == e && x.step == t;
         });
@@ -1854,23 +1882,38 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         }
       }
       // prefetches for layer l+1 (issued at gate start, pipeline.py:414-417)
-      for (int i = 0; i < m.n_pf; ++i)
-        ch.pending.push_back(Transfer{0, t, l + 1, m.pf_e[i], m.pf_bits_each[i], m.pf_b[i], m.pf_g[i], -1, -1});
+      for (int i = 0; i < n_pf && status == FATE_OK; ++i) {
+        if ((status = msg_word(&m.pf[i], processed, &w))) break;
+        ch.pending.push_back(Transfer{0, t, l + 1, msg_e(w), pf_bits, msg_b(w), msg_g(w), -1, -1});
+      }
       // on-demand loads for this step, promoted ahead of every prefetch (unless
       // already submitted when the set was posted)
-      if (od_sent != processed)
-        for (int i = 0; i < m.n_od; ++i)
-          ch.pending.push_back(Transfer{1, t, l, m.od_e[i], m.od_bits, m.od_b[i], m.od_g[i], -1, -1});
+      if (od_sent != processed && status == FATE_OK) {
+        const uint64_t oh = *(volatile uint64_t *)&m.od_head;
+        const bool posted = (uint32_t)(oh >> 32) == (uint32_t)processed + 1u;
+        const int n_od = posted ? (int)((oh >> 23) & 0x1FF) : 0, od_bits = (int)((oh >> 18) & 31);
+        for (int i = 0; i < n_od && status == FATE_OK; ++i) {
+          if ((status = msg_word(&m.od[i], processed, &w))) break;
+          ch.pending.push_back(Transfer{1, t, l, msg_e(w), od_bits, msg_b(w), msg_g(w), -1, -1});
+        }
+      }
+      if (status) break;
       ch.promote();
-      if (!m.self_signaled && !overlap) {
+      if (!self_signaled && !overlap) {
         // the compute stream may proceed once every needed transfer landed:
         // attach the signal to the last needed one still queued, else signal
         // behind everything already submitted.
+        int need_e[EMAX];
+        for (int j = 0; j < n_need && status == FATE_OK; ++j) {
+          status = msg_word(&m.need[j], processed, &w);
+          need_e[j] = msg_e(w);
+        }
+        if (status) break;
         int last = -1;
         for (int i = 0; i < (int)ch.pending.size(); ++i) {
           const Transfer &x = ch.pending[i];
           bool need = x.kind == 1 && x.layer == l && x.step == t;
-          for (int j = 0; !need && j < m.n_need; ++j) need = x.kind == 0 && x.layer == l && x.expert == m.need_e[j];
+          for (int j = 0; !need && j < n_need; ++j) need = x.kind == 0 && x.layer == l && x.expert == need_e[j];
           if (need) last = i;
         }
         if (last >= 0) {
@@ -1881,9 +1924,8 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         }
       }
       if (dbg)
-        fprintf(stderr, "[fate] msg step=%d t=%d l=%d self=%d od=%d need=%d drop=%d pf=%d pending=%zu inflight=%zu\n",
-                processed, t, l, m.self_signaled, m.n_od, m.n_need, m.n_drop, m.n_pf, ch.pending.size(),
-                ch.inflight.size());
+        fprintf(stderr, "[fate] msg step=%d t=%d l=%d self=%d need=%d drop=%d pf=%d pending=%zu inflight=%zu\n",
+                processed, t, l, (int)self_signaled, n_need, n_drop, n_pf, ch.pending.size(), ch.inflight.size());
       ++processed;
       last_progress = std::chrono::steady_clock::now();
       if ((status = ch.pump())) break;
@@ -1892,7 +1934,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     // (not between the two halves of a step's message: queued prefetches of this
     // step may still be dropped)
     if (od_sent != processed && (status = ch.pump())) break;
-    if (m.seq != (uint32_t)processed + 1u) {
+    if (!head_ok) {
       _mm_pause();
       const cudaError_t qe = cudaStreamQuery(cs);
       if (qe != cudaSuccess && qe != cudaErrorNotReady) {

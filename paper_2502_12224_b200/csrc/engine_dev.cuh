@@ -41,6 +41,29 @@ struct StepMsg {
 
 constexpr int kRing = 64;
 
+// Decode step message, device -> host (mapped pinned memory), as
+// self-validating 64-bit words: every word carries a tag of its step, so the
+// host accepts each word once its tag matches and K1 needs no system-scope
+// fence (an aligned 8-byte store arrives whole).  A run starts from a zeroed
+// ring; tags are never zero.
+//   od_head: [63:32] step+1  [31:23] n_od  [22:18] od_bits
+//   head:    [63:33] (step+1) mod 2^31  [32:24] n_need  [23:15] n_drop
+//            [14:6] n_pf  [5:1] pf_bits  [0] self_signaled
+//   entries: [63:56] entry tag  [55:48] expert  [47:32] buffer  [31:0] generation
+struct DecodeMsg {
+  uint64_t od_head;
+  uint64_t head;
+  uint64_t od[KMAX];
+  uint64_t need[KMAX];
+  uint64_t drop[EMAX];
+  uint64_t pf[EMAX];
+};
+__host__ __device__ inline uint32_t msg_entry_tag(int step) { return ((uint32_t)(step + 1) & 0x7Fu) | 0x80u; }
+__host__ __device__ inline uint64_t msg_entry(int step, int e, int b, uint32_t g) {
+  return ((uint64_t)msg_entry_tag(step) << 56) | ((uint64_t)(e & 0xFF) << 48) | ((uint64_t)(b & 0xFFFF) << 32) | g;
+}
+__host__ __device__ inline uint32_t msg_head_tag(int step) { return (uint32_t)(step + 1) & 0x7FFFFFFFu; }
+
 // Control block for the step sequence.
 struct Ctrl {
   int32_t next_token;
@@ -91,7 +114,8 @@ struct EngineDev {
   double *logits;             // [2E]
   float *x;                   // x in the four chunk-transposed K3 layouts (write_xlay)
   FfnBatch *batch;
-  StepMsg *ring;              // mapped pinned [kRing]
+  StepMsg *ring;              // mapped pinned [kRing] (prefill)
+  DecodeMsg *dring;           // mapped pinned [kRing] (decode)
 };
 
 }  // namespace fate

@@ -1027,7 +1027,7 @@ cudaError_t launch_ffn_decode_engine(const FfnBatch *batch_dev, const float *xla
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = getenv("FATE_K3_NONCOOP") ? 0 : 1;  // experiment toggle
+  cfg.numAttrs = 1;
   if (H == 2048) return cudaLaunchKernelEx(&cfg, ffn_kernel<2048>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
   if (H == 4096) return cudaLaunchKernelEx(&cfg, ffn_kernel<4096>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
   return cudaLaunchKernelEx(&cfg, ffn_kernel<0>, batch_dev, xl, part, bar, y_dev, stat, landed, abort, st);
