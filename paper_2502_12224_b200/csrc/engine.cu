@@ -180,6 +180,10 @@ __device__ void apply_prev_update(const EngineDev &d, ArcLayer *arc_sm, fate_ste
   __syncwarp();
 }
 
+#ifdef FATE_PROF
+__device__ unsigned long long g_k1_upd[4];
+__device__ __forceinline__ unsigned long long gtime1();
+#endif
 // update_after_layer of the step K1 is deciding (cache.py:212-215), by warp 1
 // of K1's tail block once warp 0 has made every free-stack edit of the step:
 // ARC accesses in ascending id order over the layer's lists (copied into
@@ -192,6 +196,9 @@ __device__ void apply_step_update(const EngineDev &d, ArcLayer *arc_sm, const in
   WarpArc arc;
   arc.attach(arc_sm);
   int nrel = 0, nvic = 0;
+#ifdef FATE_PROF
+  const unsigned long long u0 = gtime1();
+#endif
   for (int i = 0; i < k; ++i) {
     const int e = chosen[i];
     int victim;
@@ -219,7 +226,14 @@ __device__ void apply_step_update(const EngineDev &d, ArcLayer *arc_sm, const in
     }
     __syncwarp();
   }
+#ifdef FATE_PROF
+  const unsigned long long u1 = gtime1();
+#endif
   arc.store(&d.arc[layer]);
+#ifdef FATE_PROF
+  const unsigned long long u2 = gtime1();
+  if (lane == 0) g_k1_upd[0] += u1 - u0, g_k1_upd[1] += u2 - u1, g_k1_upd[2] += 1;
+#endif
   if (lane == 0) {
     Ctrl &C = *d.ctrl;
     for (int r = 0; r < nrel; ++r) {
@@ -1969,6 +1983,12 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     if (acc[6])
       fprintf(stderr, "[fate] K1 warp-1 ARC update from K1 block start: begins %.2f us, ends %.2f us\n",
               acc[4] * 1e-3 / acc[6], acc[5] * 1e-3 / acc[6]);
+    unsigned long long upd[4] = {0, 0, 0, 0};
+    cudaMemcpyFromSymbol(upd, g_k1_upd, sizeof(upd));
+    cudaMemcpyToSymbol(g_k1_upd, z, sizeof(upd));
+    if (upd[2])
+      fprintf(stderr, "[fate] K1 warp-1 ARC update: accesses %.2f us, list store %.2f us\n", upd[0] * 1e-3 / upd[2],
+              upd[1] * 1e-3 / upd[2]);
 #endif
     fprintf(stderr, "[fate] device us/step: K3 tail after its last gate opened %.2f (%llu launches waited); "
             "K3 last CTA end -> K1 block start %.2f; K1 block start -> message posted %.2f; "
