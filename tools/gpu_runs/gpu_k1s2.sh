@@ -1,0 +1,8 @@
+# K1 phase stamps after the fence-free message (profiling build), all-resident
+set -x
+mkdir -p gpurun_out
+FATE_PROF=1 python -m paper_2502_12224_b200.build --force > gpurun_out/s2_build.log 2>&1
+timeout 300 python tools/profile_kernels.py allhit 64 2>&1 | grep -v "^ " | tail -3 > gpurun_out/s2_allhit.log
+FATE_HOSTPROF=1 timeout 300 python tools/k1_probe.py 0:r 0:c > gpurun_out/s2_probe.log 2>&1
+python -m paper_2502_12224_b200.build --force >> gpurun_out/s2_build.log 2>&1
+exit 0
