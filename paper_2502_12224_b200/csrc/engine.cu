@@ -705,7 +705,8 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     // (7) self-signal when nothing must be waited for + (8) the step message
     // head (the entries carry their own tags: no fence)
     if (all_landed) ready_host[layer] = (uint32_t)token + 1u;
-    st_sys64(&msg->head, ((uint64_t)msg_head_tag(step) << 33) | ((uint64_t)n_need << 24) | ((uint64_t)n_drop << 15) |
+    st_sys64(&msg->head, ((uint64_t)msg_head_tag(step) << 38) | ((uint64_t)n_od << 33) | ((uint64_t)n_need << 24) |
+                             ((uint64_t)n_drop << 15) |
                              ((uint64_t)n_pf << 6) | ((uint64_t)(d.prefetch_bits & 31) << 1) | (all_landed ? 1u : 0u));
     // (9) control block for the next step
     C.cur_token = token;
@@ -1777,7 +1778,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       last_beat = std::chrono::steady_clock::now();
       fprintf(stderr, "[fate] beat processed=%d launched=%d pending=%zu inflight=%zu submitted=%u copy_done=%u seq=%u\n",
               processed, launched, ch.pending.size(), ch.inflight.size(), ch.submitted, *g->copy_done_host,
-              (unsigned)(g->dring_host[processed % kRing].head >> 33));
+              (unsigned)(g->dring_host[processed % kRing].head >> 38));
     }
     // profiling mode (FATE_PROFILE_SERIAL, e.g. under ncu, which serializes
     // launches): K3 of a step is enqueued only after the host has serviced that
@@ -1858,7 +1859,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     // service the step message of the next unprocessed step
     DecodeMsg &m = g->dring_host[processed % kRing];
     const uint64_t head = *(volatile uint64_t *)&m.head;
-    const bool head_ok = (uint32_t)(head >> 33) == msg_head_tag(processed);
+    const bool head_ok = (uint32_t)(head >> 38) == msg_head_tag(processed);
     // arrival-gated: the on-demand copies start as soon as K1 posts the set
     // (they go ahead of every queued prefetch, as promote_ondemand orders them)
     if (overlap && od_sent != processed && !head_ok) {
@@ -1881,6 +1882,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       const int t = processed / L, l = processed % L;
       const int n_need = (int)((head >> 24) & 0x1FF), n_drop = (int)((head >> 15) & 0x1FF);
       const int n_pf = (int)((head >> 6) & 0x1FF), pf_bits = (int)((head >> 1) & 31);
+      const int n_od_h = (int)((head >> 33) & 31);
       const bool self_signaled = head & 1u;
       uint64_t w;
       // drop queued prefetches for this step that the gate did not choose
@@ -1902,10 +1904,20 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
       }
       // on-demand loads for this step, promoted ahead of every prefetch (unless
       // already submitted when the set was posted)
-      if (od_sent != processed && status == FATE_OK) {
-        const uint64_t oh = *(volatile uint64_t *)&m.od_head;
-        const bool posted = (uint32_t)(oh >> 32) == (uint32_t)processed + 1u;
-        const int n_od = posted ? (int)((oh >> 23) & 0x1FF) : 0, od_bits = (int)((oh >> 18) & 31);
+      if (od_sent != processed && n_od_h > 0 && status == FATE_OK) {
+        // od_head may still be on its way (the head can overtake it)
+        uint64_t oh = 0;
+        for (long spin = 0;; ++spin) {
+          oh = *(volatile uint64_t *)&m.od_head;
+          if ((uint32_t)(oh >> 32) == (uint32_t)processed + 1u) break;
+          if (spin > (1l << 28)) {
+            status = FATE_ETIMEOUT;
+            set_error("fate_engine_decode: a step's on-demand set never arrived");
+            break;
+          }
+          _mm_pause();
+        }
+        const int n_od = status == FATE_OK ? n_od_h : 0, od_bits = (int)((oh >> 18) & 31);
         for (int i = 0; i < n_od && status == FATE_OK; ++i) {
           if ((status = msg_word(&m.od[i], processed, &w))) break;
           ch.pending.push_back(Transfer{1, t, l, msg_e(w), od_bits, msg_b(w), msg_g(w), -1, -1});
@@ -1936,6 +1948,22 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
         } else {
           ch.pending.push_front(Transfer{2, t, l, -1, 0, -1, 0, t, l});
         }
+      }
+      {
+        // clear every word of this step's message: a slot's entries are reused 64
+        // steps later, and an entry tag only has 7 bits of step, so a stale word
+        // must never be left for a later step to mistake for its own
+        const int n_od_w = n_od_h;
+        volatile uint64_t *vm = reinterpret_cast<volatile uint64_t *>(&m);
+        auto clear = [&](const uint64_t *w, int n) {
+          for (int i = 0; i < n; ++i) vm[&w[i] - reinterpret_cast<const uint64_t *>(&m)] = 0;
+        };
+        clear(m.od, n_od_w);
+        clear(m.need, n_need);
+        clear(m.drop, n_drop);
+        clear(m.pf, n_pf);
+        vm[0] = 0;  // od_head
+        vm[1] = 0;  // head
       }
       if (dbg)
         fprintf(stderr, "[fate] msg step=%d t=%d l=%d self=%d need=%d drop=%d pf=%d pending=%zu inflight=%zu\n",

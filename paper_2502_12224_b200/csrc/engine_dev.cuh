@@ -47,8 +47,12 @@ constexpr int kRing = 64;
 // fence (an aligned 8-byte store arrives whole).  A run starts from a zeroed
 // ring; tags are never zero.
 //   od_head: [63:32] step+1  [31:23] n_od  [22:18] od_bits
-//   head:    [63:33] (step+1) mod 2^31  [32:24] n_need  [23:15] n_drop
+//   head:    [63:38] (step+1) mod 2^26  [37:33] n_od  [32:24] n_need  [23:15] n_drop
 //            [14:6] n_pf  [5:1] pf_bits  [0] self_signaled
+// (the two heads may reach the host in either order: the head repeats n_od so
+// the host knows whether to wait for od_head).  The host clears every word it
+// consumed, so a slot never holds a stale word a later step could take for its
+// own (entry tags only carry 7 bits of the step).
 //   entries: [63:56] entry tag  [55:48] expert  [47:32] buffer  [31:0] generation
 struct DecodeMsg {
   uint64_t od_head;
@@ -62,7 +66,7 @@ __host__ __device__ inline uint32_t msg_entry_tag(int step) { return ((uint32_t)
 __host__ __device__ inline uint64_t msg_entry(int step, int e, int b, uint32_t g) {
   return ((uint64_t)msg_entry_tag(step) << 56) | ((uint64_t)(e & 0xFF) << 48) | ((uint64_t)(b & 0xFFFF) << 32) | g;
 }
-__host__ __device__ inline uint32_t msg_head_tag(int step) { return (uint32_t)(step + 1) & 0x7FFFFFFFu; }
+__host__ __device__ inline uint32_t msg_head_tag(int step) { return (uint32_t)(step + 1) & 0x3FFFFFFu; }
 
 // Control block for the step sequence.
 struct Ctrl {
