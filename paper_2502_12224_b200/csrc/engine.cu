@@ -1773,6 +1773,7 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
   const int rows_pred = g->cfg.use_predictor && g->cfg.policy != 2 ? 2 : 1;  // EAP needs no W_{l+1} rows
   const bool dbg = getenv("FATE_DEBUG") != nullptr;
   auto last_beat = std::chrono::steady_clock::now();
+  unsigned idle_spins = 0;
   while (processed < n_steps) {
     if (dbg && std::chrono::steady_clock::now() - last_beat > std::chrono::seconds(2)) {
       last_beat = std::chrono::steady_clock::now();
@@ -1978,6 +1979,9 @@ extern "C" int fate_engine_decode(fate_engine *g, const double *gate_in_dev, con
     if (od_sent != processed && (status = ch.pump())) break;
     if (!head_ok) {
       _mm_pause();
+      // the fault / watchdog checks cost a driver call: every 256th idle spin, so
+      // the poll for the next message word stays a few hundred ns
+      if ((++idle_spins & 255u) != 0u) continue;
       const cudaError_t qe = cudaStreamQuery(cs);
       if (qe != cudaSuccess && qe != cudaErrorNotReady) {
         status = cuda_status(qe, "decode compute stream (device fault)");
