@@ -702,6 +702,14 @@ __global__ void __launch_bounds__(kGateThreads) decode_gate_kernel(EngineDev d, 
     B.n = n;
     B.total_I = off;
     B.work = 0u;
+    {
+      // K3 prefetches the router rows the next step's K1 reads (W of its layer
+      // and the next one) into L2 while its CTAs gather at the final barrier
+      const int nl = layer + 1 < L ? layer + 1 : 0;
+      const int nrows = nl + 1 < L ? 2 : 1;
+      B.pf_ptr = d.W + (int64_t)nl * E * H;
+      B.pf_bytes = (unsigned long long)nrows * E * H * 8ull;
+    }
     // (7) self-signal when nothing must be waited for + (8) the step message
     // head (the entries carry their own tags: no fence)
     if (all_landed) ready_host[layer] = (uint32_t)token + 1u;

@@ -119,6 +119,10 @@ struct FfnBatch {
   int H;
   int total_I;
   unsigned int work;   // unused (kept zero)
+  // optional L2 prefetch issued by the CTAs as they reach the final barrier
+  // (the engine: the next decode step's router rows); pf_bytes % 16 == 0
+  const void *pf_ptr;
+  unsigned long long pf_bytes;
   FfnExpert e[kMaxFfnExperts];
 };
 static_assert(sizeof(FfnBatch) % 16 == 0, "K3 copies the batch with 16-byte loads");

@@ -875,6 +875,17 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const FfnBatch *__rest
   consumer_sync();
   if (ctid == 0) {
     K3_PROF(4);
+    if (batch.pf_bytes) {
+      // this CTA's share of the L2 prefetch (the next step's router rows), issued
+      // while the grid gathers at the barrier
+      const unsigned long long per = (batch.pf_bytes / G + 15ull) & ~15ull;
+      const unsigned long long off = per * blockIdx.x;
+      if (off < batch.pf_bytes) {
+        const unsigned long long n = batch.pf_bytes - off < per ? batch.pf_bytes - off : per;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                         reinterpret_cast<const uint8_t *>(batch.pf_ptr) + off), "r"((uint32_t)n) : "memory");
+      }
+    }
     grid_barrier(bar);
     K3_PROF(5);
     // every producer's waits preceded stages its CTA consumed before the barrier
